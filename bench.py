@@ -1,0 +1,336 @@
+"""Benchmark: solved instances/s of the batched Dinkelbach/SCA-Lagrangian EE
+solver (BASELINE.json metric) on N B200s, one process per GPU.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c1] [--impl b200|reference]
+
+A step = one full solve (Dinkelbach outer loop, SCA rounds, sweeps, repair,
+feasibility, binaries) of one batch of independent channel realisations.
+Weak scaling: every rank solves its own batch of distinct draws (draw index
+rank*B + i), no collective on the data path; timing is max over ranks.
+
+`value` is device-timed with inputs resident in HBM; `e2e` goes through the
+public API (`solve_batch`) from host numpy gamma with the H2D copy of inputs
+and the D2H copy of the allocation + scalars inside the timed region.  The
+CPU baseline is the oracle port (oracle/hcran_oracle.py, the numpy
+restatement of the reference) on the host cores, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1803_07772_b200.scenarios import WORKLOADS, workload_batch  # noqa: E402
+
+METRIC = "solved instances/sec (RxNxK, batch)"
+UNIT = "instances/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c4"])
+    ap.add_argument("--batch", type=int, default=None, help="instances per GPU (default: config's)")
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="instances in the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(name, batch):
+    m_f, k, ks, n, bw, _ = WORKLOADS[name]
+    desc = {"workload": f"{name}: BASELINE.json configs[{name[1]}]",
+            "rrh": m_f + 1, "users": k, "subcarriers": n, "batch_per_gpu": batch,
+            "seed": 1, "draws": "rank*batch + i",
+            "builder_pinned": {"bandwidth_hz": bw, "streaming_users": ks},
+            "l2": "flushed between timed steps (256 MiB write)"}
+    if name == "c4":
+        desc["builder_pinned"]["streaming_users"] = "0/1 (30%)"
+        desc["mode"] = "fixed-e inner solve"
+    return desc
+
+
+# ---------------------------------------------------------------- CPU side
+def _oracle_one(args):
+    name, draw = args
+    from oracle import hcran_oracle as O
+    from paper_1803_07772_b200.scenarios import workload_instance
+    cfg, ch, e = workload_instance(name, draw)
+    P = O.Prob.from_config(cfg, ch)
+    try:
+        if e is not None:
+            O.solve_fixed_e(P, e)
+        else:
+            O.dinkelbach(P)
+    except (O.Infeasible, O.ProductsActive):
+        pass
+    return draw
+
+
+def cpu_rate(name, sample, first_draw=0):
+    """Oracle port over `sample` draws on all host cores; returns (inst/s, cores, wall)."""
+    from concurrent.futures import ProcessPoolExecutor
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("MKL_NUM_THREADS", "1")
+    cores = os.cpu_count() or 1
+    tasks = [(name, first_draw + i) for i in range(sample)]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=min(cores, sample)) as pool:
+        list(pool.map(_oracle_one, tasks, chunksize=1))
+    wall = time.perf_counter() - t0
+    return sample / wall, min(cores, sample), wall
+
+
+DEFAULT_CPU_SAMPLE = {"c0": 256, "c1": 32, "c2": 8, "c4": 1024}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    name = args.config
+    sample = args.cpu_sample or DEFAULT_CPU_SAMPLE[name]
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_rate(name, min(sample, os.cpu_count() or 1), first_draw=10_000)
+    rates, walls = [], []
+    for s in range(args.steps):
+        r, cores, w = cpu_rate(name, sample, first_draw=s * sample)
+        rates.append(r)
+        walls.append(w)
+    total = sum(walls)
+    value = args.steps * sample / total
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference instance generator, seed 1)",
+            "config": workload_desc(name, sample), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{sample} draws of {name} per step, oracle/hcran_oracle.py "
+                                       f"(numpy restatement of the reference) in a "
+                                       f"{cores}-process pool on {cpu_model()}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    """Pipe peaks: MEASURED_PEAKS.json has HBM/bf16 only, so the FP64 peak is our
+    own microbenchmark (tools/peaks.cu, committed under profiles/) when present."""
+    for path in (os.path.join(ROOT, "profiles", "peaks_b200.json"),):
+        if os.path.exists(path):
+            with open(path) as f:
+                d = json.load(f)
+            return float(d["fp64_fma_tflops"]), f"measured (tools/peaks.cu, {os.path.relpath(path, ROOT)})"
+    return 37.2, "fallback: nominal 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
+def run_b200(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_1803_07772_b200 import solve_batch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    name = args.config
+    B = args.batch or WORKLOADS[name][5]
+    fixed = name == "c4"
+    batch = workload_batch(name, range(rank * B, (rank + 1) * B))
+    cfg = batch.cfg
+    kw = dict(mode="fixed_e", e_fixed=batch.e_fixed) if fixed else {}
+    el, mr = batch.elastic, batch.min_rates
+    g_dev = torch.from_numpy(batch.gamma).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(gamma, outputs=None):
+        return solve_batch(cfg, gamma, batch.sigma, el, mr, device=dev, sync=False,
+                           outputs=outputs, **kw)
+
+    for _ in range(args.warmup):
+        out = step(g_dev)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+    work = 0.0
+    outs = []
+    for s in range(args.steps):
+        flush.random_(0, 255)  # L2 flush between timed steps (outside the events)
+        ev[s][0].record(stream)
+        out = step(g_dev)
+        ev[s][1].record(stream)
+        launches += out["launches"]
+        outs.append(out)
+    barrier()
+    clocks = sampler.stop()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t_dev = sum(ms) / 1e3
+    for out in outs:
+        work += float(out["work"].sum().item())
+    sweeps = float(outs[-1]["sweeps"].double().mean().item())
+    st = outs[-1]["status"].cpu().numpy()
+    t_max = torch.tensor([t_dev], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_all = float(t_max.item())
+    value = world * B * args.steps / t_all
+
+    # end-to-end through the public API: host gamma in, allocation + scalars out
+    e2e = None
+    if not args.no_e2e:
+        want = ["p", "ee", "total_power", "status", "rho", "a", "launches"]
+        h2d = batch.gamma.nbytes + el.size + mr.nbytes
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        d2h = 0
+        for s in range(args.steps):
+            o = step(batch.gamma, outputs=want)
+            res = {k: v.cpu() for k, v in o.items() if hasattr(v, "cpu") and not k.startswith("_")}
+            d2h = sum(v.numel() * v.element_size() for v in res.values())
+        t1.record(stream)
+        barrier()
+        te = torch.tensor([t0.elapsed_time(t1) / 1e3], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * args.steps / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        achieved = work / t_dev / 1e12  # rank 0's own launches and time
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference instance generator: users in a 500 m disc, "
+                        "Rayleigh x d^-3 gains, seed 1)",
+                "config": workload_desc(name, B),
+                "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
+                             "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                             "peak_source": peak_src,
+                             "note": "algorithmic FP64 flop-equivalents counted by the kernel "
+                                     "(DESIGN.md work model) / device time of the solve"},
+                "gpu_launches": launches, "clocks": clocks, "e2e": e2e,
+                "solver": {"mean_sweeps_per_instance": sweeps,
+                           "status_counts": {str(k): int(v) for k, v in
+                                             zip(*np.unique(st, return_counts=True))}}}
+        if world == 1 and not args.no_cpu_baseline:
+            sample = args.cpu_sample or DEFAULT_CPU_SAMPLE[name]
+            r, cores, wall = cpu_rate(name, sample)
+            line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
+                                    "sample": f"{sample} draws of {name} ({wall:.1f} s), "
+                                              f"oracle/hcran_oracle.py in a {cores}-process pool "
+                                              f"on {cpu_model()}"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_b200(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,151 @@
+/*
+ * hcran_b200.h -- C ABI of the B200 batched EE solver (libhcran_b200.so).
+ *
+ * Drop-in boundary for the reference's hot path.  The
+ * reference (hcran-noma, pure Python) has no native ABI; these entry points
+ * replace, for a whole batch of independent channel realisations at once:
+ *
+ *   hcran_b200_solve_batch          <- dinkelbach.solve(ch, cfg, ScaleSolver())
+ *                                      /root/reference/pkg/src/hcran_noma/dinkelbach.py:65-112
+ *                                      fanned out by scenarios.run_sweep / run_draw
+ *                                      (scenarios.py:237-296)
+ *   hcran_b200_solve_fixed_e_batch  <- ScaleSolver.solve_fixed_e(ch, cfg, e, warm_start)
+ *                                      (scale.py:506-551; the InnerSolver protocol,
+ *                                      dinkelbach.py:28-33)
+ *   hcran_b200_plan                 <- (no reference counterpart: workspace sizing)
+ *   hcran_b200_version              <- hcran_noma.__version__ (__init__.py:36)
+ *
+ * Conventions: plain C types only; every array pointer is DEVICE memory owned
+ * by the caller; arrays are row-major with the reference's [m][k][n] =
+ * (RRH, user, subcarrier) index order (model.py:8-11).  Calls are
+ * stream-ordered (`stream` is a cudaStream_t, NULL = legacy default), never
+ * allocate, never synchronise the host, and are thread-safe across distinct
+ * (stream, workspace) pairs.  Return value: 0 on success, a negative
+ * HCRAN_E_* code on argument errors (nothing is launched then).  Per-instance
+ * outcomes are reported through `status` (HCRAN_ST_*), mirroring the
+ * reference's DinkelbachTrace.status / InnerResult.status / InfeasibleProblemError.
+ */
+#ifndef HCRAN_B200_H
+#define HCRAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCRAN_B200_ABI_VERSION 1
+
+/* error codes (return values) */
+#define HCRAN_OK 0
+#define HCRAN_E_ARG (-1)        /* null pointer / bad dimension */
+#define HCRAN_E_SIZE (-2)       /* M,K,N or l_max outside the supported range */
+#define HCRAN_E_WORKSPACE (-3)  /* workspace too small (see hcran_b200_plan) */
+#define HCRAN_E_LAUNCH (-4)     /* CUDA launch failure */
+
+/* per-instance status codes */
+#define HCRAN_ST_CONVERGED 0   /* Dinkelbach surplus <= xi            (dinkelbach.py:93-97)  */
+#define HCRAN_ST_CAP 1         /* outer_max reached                   (dinkelbach.py:104-106) */
+#define HCRAN_ST_STALLED 2     /* ee <= e, or a later inner infeasible (dinkelbach.py:82-102) */
+#define HCRAN_ST_INFEASIBLE 3  /* first inner solve infeasible -> InfeasibleProblemError
+                                  (dinkelbach.py:81-86); fixed-e: InnerResult "infeasible" */
+#define HCRAN_ST_OK 0          /* fixed-e: InnerResult "ok" */
+#define HCRAN_ST_UNSUPPORTED 4 /* non-exclusive seating (theta/theta' families live,
+                                  scale.py:566) -- not implemented on the device */
+
+/* Tolerances (model.py:59-80); rho1/rho2 already resolved from the mask. */
+typedef struct hcran_tolerances {
+  double xi;           /* Dinkelbach surplus stop                    */
+  double varpi1_rel;   /* sweep stop, relative to p_max[m]           */
+  double varpi2_rel;   /* round stop, relative to p_max[m]           */
+  int32_t s_max;       /* SCA rounds                                 */
+  int32_t v_max;       /* sweeps per round                           */
+  int32_t outer_max;   /* Dinkelbach iterations                      */
+  double rho1, rho2;   /* C10 / C11 product slack levels             */
+  double dual_cap;     /* multiplier cap                             */
+  double c13_rate_tol; /* streaming rate band                        */
+  double c14_rel_tol;  /* SIC margin band                            */
+  double box_rel_tol;  /* mask / budget band                         */
+} hcran_tolerances_t;
+
+/* Network configuration shared by every instance of a batch (NetworkConfig,
+ * model.py:83-185).  All arrays are device pointers. */
+typedef struct hcran_problem {
+  int32_t M, K, N;        /* RRHs, users, subcarriers                         */
+  int32_t l_max;          /* users per subcarrier (SIC cluster size)          */
+  const double* p_max;    /* [M]        per-RRH budget, W                     */
+  const double* p_mask;   /* [M][K][N]  spectral mask, W                      */
+  const double* eta;      /* [M]        amplifier inefficiency                */
+  const double* weights;  /* [M][K]     rate weights in [0, 1]                */
+  const double* sigma;    /* [M][K][N]  noise power, W                        */
+  double static_power;    /* fibre + circuit floor, W (model.py:173-176)      */
+  hcran_tolerances_t tol;
+} hcran_problem_t;
+
+/* Per-instance inputs. */
+typedef struct hcran_batch_in {
+  int64_t B;                /* instances                                      */
+  const double* gamma;      /* [B][M][K][N] channel power gains (ChannelState.gamma) */
+  const uint8_t* elastic;   /* [B][K] 1 = elastic user, 0 = streaming          */
+  const double* min_rates;  /* [B][K] minimum rate, bits/s/Hz (0 for elastic)   */
+  const double* e_fixed;    /* [B] fixed-e solves only (else ignored)          */
+  const double* warm_p;     /* [B][M][K][N] fixed-e warm start or NULL         */
+} hcran_batch_in_t;
+
+/* Per-instance outputs (any pointer may be NULL to skip that output). */
+typedef struct hcran_batch_out {
+  double* p;             /* [B][M][K][N] PowerAllocation.p, W                  */
+  uint8_t* rho;          /* [B][M][K][N] PowerAllocation.rho                   */
+  uint8_t* a;            /* [B][M][K]    PowerAllocation.a                     */
+  double* ee;            /* [B] EnergyReport.ee of the final allocation        */
+  double* sum_rate;      /* [B] EnergyReport.sum_rate                          */
+  double* total_power;   /* [B] EnergyReport.total_power                       */
+  double* final_e;       /* [B] DinkelbachTrace.final_e (fixed-e: e)           */
+  double* objective;     /* [B] R - e P of the returned allocation (true objective) */
+  int32_t* outer_iters;  /* [B] len(DinkelbachTrace.iterations)                */
+  int32_t* rounds;       /* [B] SCA rounds, summed over outer iterations       */
+  int32_t* sweeps;       /* [B] power sweeps, summed over outer iterations     */
+  int32_t* bisect_evals; /* [B] budget-multiplier load evaluations (work counter) */
+  int8_t* status;        /* [B] HCRAN_ST_*                                     */
+  uint8_t* feasible;     /* [B] check_feasibility(final).ok                    */
+  double* xi;            /* [B][M] budget multipliers at the last sweep        */
+  double* zeta;          /* [B][K] rate multipliers at the last sweep          */
+  double* e_trace;       /* [B][outer_max] Dinkelbach e per iteration (nan-padded) */
+  double* surplus_trace; /* [B][outer_max] surplus per iteration               */
+  int32_t* rounds_trace; /* [B][outer_max] rounds per outer iteration          */
+  int32_t* sweeps_trace; /* [B][outer_max] sweeps per outer iteration          */
+  uint8_t* flags;        /* [B] HCRAN_FLAG_* diagnostics                        */
+  double* work;          /* [B] algorithmic FP64 work, flop-equivalents */
+} hcran_batch_out_t;
+
+/* flags: a seat met num == den == 0 in the seated-pair SIC model, i.e. the
+ * reference would decide it from floor-level multipliers of unseated pairs
+ * (the instance is re-solved with the dense pair family). */
+#define HCRAN_FLAG_FLOOR_TIE 1
+#define HCRAN_FLAG_DENSE_RESOLVED 2 /* result comes from the dense-pair re-solve */
+
+/* Workspace sizing: number of CTAs the solver will keep resident for this
+ * problem on `device` and the device workspace bytes it needs. */
+int hcran_b200_plan(const hcran_problem_t* prob, int64_t B, int device,
+                    int32_t* grid_out, size_t* ws_bytes_out);
+
+/* Full Dinkelbach solve of every instance (device-side outer loop). */
+int hcran_b200_solve_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
+                           hcran_batch_out_t* out, void* workspace, size_t ws_bytes,
+                           void* stream);
+
+/* One fixed-e inner solve per instance (InnerSolver conformance). */
+int hcran_b200_solve_fixed_e_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
+                                   hcran_batch_out_t* out, void* workspace,
+                                   size_t ws_bytes, void* stream);
+
+/* Kernel launches issued by the last successful call on this thread. */
+int32_t hcran_b200_last_launches(void);
+
+const char* hcran_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCRAN_B200_H */

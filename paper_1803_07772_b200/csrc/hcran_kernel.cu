@@ -1,0 +1,156 @@
+// hcran_kernel.cu -- sm_100a kernel + C ABI (include/hcran_b200.h).
+//
+// Execution model: a persistent grid of CTAs (a multiple of the SM count),
+// each pulling whole channel realisations off an atomic work queue and
+// solving them start to finish (Dinkelbach outer loop, SCA rounds, sweeps,
+// repair) with the state in its own workspace slot.  Instances are
+// independent, so there is no inter-CTA communication beyond the queue
+// counter, and per-instance work imbalance (4-21 outer iterations, 60-900
+// sweeps) is absorbed by the queue.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include "hcran_solver.cuh"
+
+using namespace hcran;
+
+#ifndef HCRAN_THREADS
+#define HCRAN_THREADS 256
+#endif
+
+static __global__ void __launch_bounds__(HCRAN_THREADS)
+    hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
+  // pass 1 (v.dense == 0): every instance, seated-pair SIC family, flags floor ties.
+  // pass 2 (v.dense == 1): only instances flagged by pass 1, dense pair family.
+  __shared__ double red[2 * HCRAN_THREADS / 32];
+  __shared__ Ctl ctl;
+  __shared__ long long next;
+  DevEx ex;
+  ex.init(red);
+  Work W;
+  W.layout(ws + (size_t)blockIdx.x * per_cta, v.M, v.K, v.N, v.dense != 0);
+  Solver<DevEx> S(ex, v, W, ctl);
+  for (;;) {
+    if (threadIdx.x == 0) next = (long long)atomicAdd(counter, 1);
+    __syncthreads();
+    const long long b = next;
+    __syncthreads();
+    if (b >= v.B) break;
+    if (v.flag_in && !v.flag_in[b]) continue;
+    S.load_instance(b);
+    if (mode == 0) S.dinkelbach(b);
+    else S.fixed_e(b);
+    __syncthreads();
+  }
+}
+
+static thread_local int32_t g_last_launches = 0;
+static const size_t HEADER = 256;
+
+static int check_problem(const hcran_problem_t* p) {
+  if (!p) return HCRAN_E_ARG;
+  if (p->M < 1 || p->K < 1 || p->N < 1) return HCRAN_E_SIZE;
+  if (p->K > 255 || p->N > 256 || p->M > 31) return HCRAN_E_SIZE;
+  if (p->l_max < 1 || p->l_max > SMAX) return HCRAN_E_SIZE;
+  if (!p->p_max || !p->p_mask || !p->eta || !p->weights || !p->sigma) return HCRAN_E_ARG;
+  return HCRAN_OK;
+}
+
+static size_t per_cta_bytes(const hcran_problem_t* p, bool dense = false) {
+  Work w;
+  return w.layout(nullptr, p->M, p->K, p->N, dense);
+}
+
+static size_t flags_bytes(int64_t B) { return ((size_t)B + 255) & ~(size_t)255; }
+
+// CTAs for the dense re-solve pass: a few per SM at most, bounded to ~4 GiB of state
+static int64_t dense_ctas(const hcran_problem_t* p, int64_t B, int64_t grid1) {
+  size_t per = per_cta_bytes(p, true);
+  int64_t g = (int64_t)(((size_t)4 << 30) / per);
+  if (g > grid1) g = grid1;
+  if (g > B) g = B;
+  if (g < 1) g = 1;
+  return g;
+}
+
+static int resident_ctas(int device) {
+  int sms = 148, per_sm = 1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hcran_solve_kernel, HCRAN_THREADS, 0) !=
+          cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  if (per_sm > 4) per_sm = 4;  // state lives in the workspace: bound its footprint
+  return sms * per_sm;
+}
+
+extern "C" int hcran_b200_plan(const hcran_problem_t* prob, int64_t B, int device,
+                               int32_t* grid_out, size_t* ws_bytes_out) {
+  int rc = check_problem(prob);
+  if (rc) return rc;
+  if (B < 0 || !grid_out || !ws_bytes_out) return HCRAN_E_ARG;
+  int64_t grid = resident_ctas(device);
+  if (B < grid) grid = B > 0 ? B : 1;
+  *grid_out = (int32_t)grid;
+  *ws_bytes_out = HEADER + flags_bytes(B) + (size_t)grid * per_cta_bytes(prob) +
+                  (size_t)dense_ctas(prob, B, grid) * per_cta_bytes(prob, true);
+  return HCRAN_OK;
+}
+
+static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran_batch_out_t* out,
+                  void* workspace, size_t ws_bytes, void* stream, int mode) {
+  g_last_launches = 0;
+  int rc = check_problem(prob);
+  if (rc) return rc;
+  if (!in || !out || !workspace || !in->gamma || !in->elastic || !in->min_rates) return HCRAN_E_ARG;
+  if (mode == 1 && !in->e_fixed) return HCRAN_E_ARG;
+  if (in->B <= 0) return HCRAN_OK;
+  int device = 0;
+  cudaGetDevice(&device);
+  const size_t per = per_cta_bytes(prob), perd = per_cta_bytes(prob, true);
+  int64_t grid = resident_ctas(device);
+  if (in->B < grid) grid = in->B;
+  const int64_t grid2 = dense_ctas(prob, in->B, grid);
+  const size_t fixed = HEADER + flags_bytes(in->B) + (size_t)grid2 * perd;
+  if (ws_bytes < fixed + per) return HCRAN_E_WORKSPACE;
+  const int64_t fit = (int64_t)((ws_bytes - fixed) / per);
+  if (fit < grid) grid = fit;
+  View v;
+  v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
+  v.p_max = prob->p_max; v.mask = prob->p_mask; v.eta = prob->eta; v.w = prob->weights;
+  v.sig = prob->sigma; v.static_power = prob->static_power; v.tol = prob->tol;
+  v.B = in->B; v.gamma = in->gamma; v.elastic = in->elastic; v.min_rates = in->min_rates;
+  v.e_fixed = in->e_fixed; v.warm_p = in->warm_p; v.out = *out;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* base = (char*)workspace;
+  uint8_t* flags = (uint8_t*)(base + HEADER);
+  char* slots1 = base + HEADER + flags_bytes(in->B);
+  char* slots2 = slots1 + (size_t)grid * per;
+  if (cudaMemsetAsync(base, 0, HEADER, s) != cudaSuccess) return HCRAN_E_LAUNCH;
+  v.dense = 0; v.flag_int = flags; v.flag_in = nullptr;
+  hcran_solve_kernel<<<(unsigned)grid, HCRAN_THREADS, 0, s>>>(v, slots1, per, (int*)base, mode);
+  if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
+  v.dense = 1; v.flag_int = nullptr; v.flag_in = flags;
+  hcran_solve_kernel<<<(unsigned)grid2, HCRAN_THREADS, 0, s>>>(v, slots2, perd, (int*)base + 1,
+                                                               mode);
+  if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
+  g_last_launches = 2;
+  return HCRAN_OK;
+}
+
+extern "C" int hcran_b200_solve_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
+                                      hcran_batch_out_t* out, void* workspace, size_t ws_bytes,
+                                      void* stream) {
+  return launch(prob, in, out, workspace, ws_bytes, stream, 0);
+}
+
+extern "C" int hcran_b200_solve_fixed_e_batch(const hcran_problem_t* prob,
+                                              const hcran_batch_in_t* in, hcran_batch_out_t* out,
+                                              void* workspace, size_t ws_bytes, void* stream) {
+  return launch(prob, in, out, workspace, ws_bytes, stream, 1);
+}
+
+extern "C" int32_t hcran_b200_last_launches(void) { return g_last_launches; }
+
+extern "C" const char* hcran_b200_version(void) {
+  return "hcran_b200 0.1.0 (abi 1, sm_100a, fp64 core)";
+}

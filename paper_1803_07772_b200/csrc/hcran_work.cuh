@@ -1,0 +1,105 @@
+// hcran_work.cuh -- per-CTA workspace layout (one instance in flight per CTA).
+//
+// Dense per-cell state is [m][k][n] (cell c = (m*K + k)*N + n, the
+// reference's index order, model.py:8-11), so a (m, n) column is strided by
+// N and consecutive threads of a column phase touch consecutive n.
+// Seat-compressed state: every (m, n) column holds at most SMAX seated users
+// (exclusive seating, scale.py:561-566, 1007-1014), slots sorted by user
+// index; the SIC multiplier family lives only on seated pairs (SURVEY.md
+// 7.3-2, probe A.9: bit-identical to the dense family).
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+#include "hcran_exec.cuh"
+
+namespace hcran {
+
+constexpr int SMAX = 4;                       // seats per column (l_max <= 4)
+constexpr int NPAIR = SMAX * (SMAX - 1) / 2;  // seated pairs per column
+constexpr uint8_t NOSLOT = 0xFF;
+
+struct Work {
+  // dense [C]
+  double *p, *pacc, *alpha, *u, *ts;
+  uint8_t *ord, *rnk, *slot, *flag;
+  // columns [MN]
+  double *tot, *pcross, *fterm, *dcross, *bterm, *mtot, *colmax;
+  uint8_t *ncnt, *npr;
+  // [KN]
+  double *full, *utot, *fullm;
+  // seats [MN * SMAX]
+  double *s_plin, *s_logplin, *s_num, *s_den, *s_psis, *s_cross, *s_inv, *s_rhat, *s_dlog,
+      *s_beta, *s_dsA, *s_dsB, *s_nsS, *s_nsW, *s_dagg, *s_aagg, *s_pround;
+  uint8_t* s_user;
+  // pairs [MN * NPAIR]
+  double *pr_zt, *pr_step, *pr_gconst, *pr_gval, *pr_brk, *pr_slack;
+  uint8_t *pr_s, *pr_w;  // slot indices of strong / weak member
+  // users
+  double *zeta, *minr, *score, *urate;  // score [M*K]
+  uint8_t *elastic, *hsort, *best;      // hsort [K*M]: heads by score, descending; best [K]
+  int32_t *tried, *needy;               // boost bookkeeping [K]
+  double* dtmp;                         // [K]
+  int32_t *useat, *ucnt;                // useat [K*N]: seat id = col*SMAX + slot
+  // heads
+  double *xi, *delta, *eps1, *eps2, *mtmp;
+  int32_t* mev;  // budget-load evaluations per head (work counter)
+  // repair scratch
+  double *tb, *tX, *tY, *tS, *leaf;  // [MN] x4, leaf [C/64 + 64]
+  int32_t* perm;                     // [N]
+  // dense SIC pair family (exact mode for floor-tie instances) -- bound when dense
+  double *cx, *cxl, *dA, *dB, *nS, *nW, *dg, *ag;  // [C]
+  double *pd_zt, *pd_step;                         // [MN * K(K-1)/2]
+
+  HD static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
+
+  // returns bytes; binds pointers when base != nullptr
+  HD size_t layout(char* base, int M, int K, int N, bool dense = false) {
+    const size_t C = size_t(M) * K * N, MN = size_t(M) * N, KN = size_t(K) * N;
+    const size_t S = MN * SMAX, PP = MN * NPAIR;
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char* {
+      char* r = base ? base + off : nullptr;
+      off += align(bytes);
+      return r;
+    };
+#define HC_D(name, n) name = (double*)take(sizeof(double) * (n))
+#define HC_B(name, n) name = (uint8_t*)take(n)
+#define HC_I(name, n) name = (int32_t*)take(sizeof(int32_t) * (n))
+    HC_D(p, C); HC_D(pacc, C); HC_D(alpha, C); HC_D(u, C); HC_D(ts, C);
+    HC_B(ord, C); HC_B(rnk, C); HC_B(slot, C); HC_B(flag, C);
+    HC_D(tot, MN); HC_D(pcross, MN); HC_D(fterm, MN); HC_D(dcross, MN); HC_D(bterm, MN);
+    HC_D(mtot, MN); HC_D(colmax, MN);
+    HC_B(ncnt, MN); HC_B(npr, MN);
+    HC_D(full, KN); HC_D(utot, KN); HC_D(fullm, KN);
+    HC_D(s_plin, S); HC_D(s_logplin, S); HC_D(s_num, S); HC_D(s_den, S); HC_D(s_psis, S);
+    HC_D(s_cross, S); HC_D(s_inv, S); HC_D(s_rhat, S); HC_D(s_dlog, S); HC_D(s_beta, S);
+    HC_D(s_dsA, S); HC_D(s_dsB, S); HC_D(s_nsS, S); HC_D(s_nsW, S); HC_D(s_dagg, S);
+    HC_D(s_aagg, S); HC_D(s_pround, S);
+    HC_B(s_user, S);
+    HC_D(pr_zt, PP); HC_D(pr_step, PP); HC_D(pr_gconst, PP); HC_D(pr_gval, PP);
+    HC_D(pr_brk, PP); HC_D(pr_slack, PP);
+    HC_B(pr_s, PP); HC_B(pr_w, PP);
+    HC_D(zeta, K); HC_D(minr, K); HC_D(score, size_t(M) * K); HC_D(urate, K);
+    HC_B(elastic, K); HC_B(hsort, size_t(K) * M); HC_B(best, K);
+    HC_I(tried, K); HC_I(needy, K); HC_D(dtmp, K);
+    HC_I(useat, KN); HC_I(ucnt, K);
+    HC_D(xi, M); HC_D(delta, M); HC_D(eps1, M); HC_D(eps2, M); HC_D(mtmp, M);
+    HC_I(mev, M);
+    HC_D(tb, MN); HC_D(tX, MN); HC_D(tY, MN); HC_D(tS, MN); HC_D(leaf, C / 64 + 64);
+    HC_I(perm, N);
+    if (dense) {
+      const size_t PD = MN * (size_t(K) * (K - 1) / 2);
+      HC_D(cx, C); HC_D(cxl, C); HC_D(dA, C); HC_D(dB, C); HC_D(nS, C); HC_D(nW, C);
+      HC_D(dg, C); HC_D(ag, C);
+      HC_D(pd_zt, PD); HC_D(pd_step, PD);
+    } else {
+      cx = cxl = dA = dB = nS = nW = dg = ag = pd_zt = pd_step = nullptr;
+    }
+#undef HC_D
+#undef HC_B
+#undef HC_I
+    return off;
+  }
+};
+
+}  // namespace hcran

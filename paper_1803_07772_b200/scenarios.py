@@ -177,22 +177,24 @@ class Batch:
     gamma: np.ndarray             # (B, M, K, N) float64
     sigma: np.ndarray             # (M, K, N) float64 (flat noise: shared)
     elastic: np.ndarray           # (B, K) bool
+    min_rates: np.ndarray         # (B, K) bits/s/Hz (0 for elastic users)
     e_fixed: np.ndarray | None    # (B,) for fixed-e workloads
     draws: np.ndarray             # (B,) int64
 
 
 def workload_batch(name: str, draws, seed: int = 1) -> Batch:
     draws = np.asarray(list(draws), dtype=np.int64)
-    cfgs, gam, el, es = [], [], [], []
+    cfgs, gam, el, mr, es = [], [], [], [], []
     for d in draws:
         cfg, ch, e = workload_instance(name, int(d), seed)
         cfgs.append(cfg)
         gam.append(ch.gamma)
         el.append(cfg.elastic_mask())
+        mr.append(cfg.min_rates())
         es.append(e)
     cfg0 = cfgs[0]
     return Batch(cfg=cfg0, gamma=np.stack(gam), sigma=gen_sigma(cfg0),
-                 elastic=np.stack(el), e_fixed=None if es[0] is None else np.array(es),
+                 elastic=np.stack(el), min_rates=np.stack(mr), e_fixed=None if es[0] is None else np.array(es),
                  draws=draws)
 
 

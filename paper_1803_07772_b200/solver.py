@@ -1,0 +1,264 @@
+"""B200 solve entry points with the reference's names and result layout.
+
+Drop-in surface:
+
+* `ScaleSolver().solve_fixed_e(ch, cfg, e, warm_start)` -> `InnerResult`
+  (scale.py:489-551; the `InnerSolver` protocol of dinkelbach.py:28-33)
+* `solve(ch, cfg, inner=None)` -> `DinkelbachTrace` (dinkelbach.py:65-112),
+  with the whole outer loop on the device
+* `solve_batch(cfg, gamma, ...)` -> dict of per-instance tensors: the batched
+  form the C ABI exposes (one launch pair for the whole batch)
+
+Host code only packs arguments and moves buffers (torch is the device-memory
+and stream plumbing); all arithmetic runs in libhcran_b200.so.  There is no
+CPU fallback: without the library or a CUDA device every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi, pack
+from .model import PowerAllocation
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhcran_b200.so")
+
+
+class InfeasibleProblemError(RuntimeError):
+    """The streaming constraints cannot be met (dinkelbach.py:24-25)."""
+
+
+class B200Unavailable(RuntimeError):
+    """libhcran_b200.so or a CUDA device is missing: there is no fallback."""
+
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise B200Unavailable(f"{LIB_PATH} not built (run __graft_entry__.build())")
+        _lib = _abi.bind_device_lib(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise B200Unavailable("no CUDA device: the B200 solver has no CPU path")
+    return torch
+
+
+_TORCH_DT = {"f8": "float64", "u1": "uint8", "i4": "int32", "i1": "int8"}
+
+
+class _DeviceProblem:
+    """Batch-constant config arrays resident on the device + the C struct."""
+
+    def __init__(self, cfg, sigma, device):
+        torch = _torch()
+        arrs = pack.problem_arrays(cfg, sigma)
+        self.t = {k: torch.from_numpy(v).to(device) for k, v in arrs.items()}
+        self.struct = pack.problem_struct(cfg, {k: v.data_ptr() for k, v in self.t.items()})
+        self.shape = (cfg.n_rrh, cfg.n_users, cfg.n_subcarriers)
+
+
+def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="dinkelbach",
+                e_fixed=None, warm_p=None, stream=None, outputs=None, device=None,
+                workspace=None, sync=True):
+    """Solve every instance of a batch on the device.
+
+    cfg        template NetworkConfig (p_max, p_mask, eta, weights, l_max, tolerances)
+    gamma      (B, M, K, N) float64 channel gains: numpy (copied in) or a CUDA tensor
+    sigma      (M, K, N) noise powers (default: the config's flat noise floor)
+    elastic    (B, K) bool / min_rates (B, K): per-instance user classes (default: cfg's)
+    mode       "dinkelbach" (full solve) or "fixed_e" (one inner solve per instance)
+    outputs    subset of _abi.OUT_FIELDS names to produce (default: all)
+    Returns a dict of CUDA tensors keyed like hcran_batch_out_t (plus "launches").
+    """
+    torch = _torch()
+    lib = library()
+    dev = torch.device(device or "cuda")
+    M, K, N = cfg.n_rrh, cfg.n_users, cfg.n_subcarriers
+    if sigma is None:
+        sigma = np.full((M, K, N), cfg.noise_density * cfg.subcarrier_bandwidth)
+    prob = _DeviceProblem(cfg, sigma, dev)
+    if isinstance(gamma, np.ndarray):
+        g = torch.from_numpy(np.ascontiguousarray(gamma, np.float64)).to(dev)
+    else:
+        g = gamma.to(dev, torch.float64).contiguous()
+    B = int(g.shape[0])
+    if elastic is None:
+        elastic = np.broadcast_to(cfg.elastic_mask(), (B, K))
+    if min_rates is None:
+        min_rates = np.broadcast_to(cfg.min_rates(), (B, K))
+    el = torch.as_tensor(np.ascontiguousarray(elastic, np.uint8)).to(dev)
+    mr = torch.as_tensor(np.ascontiguousarray(min_rates, np.float64)).to(dev)
+    ef = None
+    if mode == "fixed_e":
+        ef = torch.as_tensor(np.ascontiguousarray(np.broadcast_to(e_fixed, (B,)), np.float64)).to(dev)
+    wp = None
+    if warm_p is not None:
+        wp = torch.as_tensor(np.ascontiguousarray(warm_p, np.float64)).to(dev)
+    T = cfg.tolerances.outer_max
+    outs = {}
+    for name, dt, kind in _abi.OUT_FIELDS:
+        if outputs is not None and name not in outputs:
+            continue
+        outs[name] = torch.empty(_abi.out_shape(kind, B, M, K, N, T),
+                                 dtype=getattr(torch, _TORCH_DT[dt]), device=dev)
+    bi = _abi.BatchIn(B=B, gamma=g.data_ptr(), elastic=el.data_ptr(), min_rates=mr.data_ptr(),
+                      e_fixed=ef.data_ptr() if ef is not None else None,
+                      warm_p=wp.data_ptr() if wp is not None else None)
+    bo = _abi.BatchOut(**{k: v.data_ptr() for k, v in outs.items()})
+    grid, wsb = C.c_int32(), C.c_size_t()
+    rc = lib.hcran_b200_plan(C.byref(prob.struct), B, dev.index or 0, C.byref(grid), C.byref(wsb))
+    if rc:
+        raise ValueError(f"hcran_b200_plan: {_abi.ERRORS.get(rc, rc)}")
+    if workspace is None or workspace.numel() < wsb.value:
+        workspace = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    fn = lib.hcran_b200_solve_batch if mode == "dinkelbach" else lib.hcran_b200_solve_fixed_e_batch
+    rc = fn(C.byref(prob.struct), C.byref(bi), C.byref(bo), workspace.data_ptr(), wsb.value,
+            s.cuda_stream)
+    if rc:
+        raise RuntimeError(f"hcran_b200 solve failed: {_abi.ERRORS.get(rc, rc)}")
+    outs["launches"] = int(lib.hcran_b200_last_launches())
+    outs["_keepalive"] = (prob, g, el, mr, ef, wp, workspace)
+    if sync:
+        s.synchronize()
+    return outs
+
+
+# --------------------------------------------------------------------------
+# reference-shaped results
+# --------------------------------------------------------------------------
+
+@dataclass
+class SolveStats:
+    """Mirrors scale.SolveStats (scale.py:405-418) for the fields the device reports."""
+    status: str = "ok"
+    rounds: int = 0
+    total_sweeps: int = 0
+    true_objective: float = float("nan")
+    used_warm_start: bool = False
+    infeasible_reason: str | None = None
+    budget_evals: int = 0
+    flags: int = 0
+    round_objectives: list = field(default_factory=list)
+
+
+@dataclass
+class InnerResult:
+    allocation: PowerAllocation
+    status: str
+    stats: SolveStats
+
+
+@dataclass(frozen=True)
+class DinkelbachIteration:
+    e: float
+    surplus: float
+    inner_stats: object
+
+
+@dataclass
+class DinkelbachTrace:
+    iterations: list = field(default_factory=list)
+    final_e: float = 0.0
+    final_allocation: PowerAllocation | None = None
+    cap_hit: bool = False
+    status: str = "converged"
+    xi: np.ndarray | None = None
+    zeta: np.ndarray | None = None
+
+    @property
+    def e_values(self) -> list[float]:
+        return [it.e for it in self.iterations]
+
+
+def _host(outs: dict) -> dict:
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v)
+            for k, v in outs.items() if not k.startswith("_")}
+
+
+class ScaleSolver:
+    """B200 inner solver with the reference's InnerSolver interface.
+
+    `solve_fixed_e` runs one fixed-e solve (scale.py:506-551) on the device;
+    `solve(ch, cfg, ScaleSolver())` runs the whole Dinkelbach loop on the
+    device.  Constructor knobs of the reference (workers, collect_trace, gains,
+    damping, min_sweeps, multistart_cells) are accepted for drop-in
+    compatibility; only the reference defaults are implemented on device."""
+
+    def __init__(self, workers: int = 1, collect_trace: bool = False,
+                 gains=(0.6, 0.8, 0.6, 0.6, 0.6), damping: float = 1.0, min_sweeps: int = 8,
+                 multistart_cells: int = 16, device=None):
+        if tuple(gains) != (0.6, 0.8, 0.6, 0.6, 0.6) or damping != 1.0 or min_sweeps != 8:
+            raise NotImplementedError("the B200 solver implements the reference defaults only")
+        self.device = device
+
+    def solve_fixed_e(self, ch, cfg, e: float, warm_start: PowerAllocation | None = None):
+        if e < 0:
+            raise ValueError("the efficiency parameter must be non-negative")
+        warm = None if warm_start is None else np.asarray(warm_start.p, np.float64)[None]
+        o = _host(solve_batch(cfg, np.asarray(ch.gamma)[None], np.asarray(ch.sigma),
+                              mode="fixed_e", e_fixed=float(e), warm_p=warm,
+                              device=self.device))
+        st = int(o["status"][0])
+        status = _abi.HCRAN_ST_FIXED.get(st, "infeasible")
+        stats = SolveStats(status=status, rounds=int(o["rounds"][0]),
+                           total_sweeps=int(o["sweeps"][0]),
+                           used_warm_start=warm_start is not None,
+                           budget_evals=int(o["bisect_evals"][0]), flags=int(o["flags"][0]))
+        if st == 4:
+            raise NotImplementedError("non-exclusive seating (products-active families)")
+        alloc = PowerAllocation(p=o["p"][0].copy())
+        if status == "ok":
+            alloc.rho, alloc.a = o["rho"][0].copy(), o["a"][0].copy()
+            stats.true_objective = float(o["objective"][0])
+        else:
+            stats.infeasible_reason = "repair could not meet the streaming rates"
+        return InnerResult(alloc, status, stats)
+
+
+def solve(ch, cfg, inner=None, e0: float = 0.0) -> DinkelbachTrace:
+    """dinkelbach.solve with the outer loop on the device (dinkelbach.py:65-112)."""
+    if inner is not None and not isinstance(inner, ScaleSolver):
+        raise TypeError("the B200 Dinkelbach loop runs on the device with the B200 ScaleSolver")
+    if e0 != 0.0:
+        raise NotImplementedError("the device loop starts from e0 = 0 (the reference default)")
+    dev = inner.device if inner is not None else None
+    o = _host(solve_batch(cfg, np.asarray(ch.gamma)[None], np.asarray(ch.sigma), device=dev))
+    return trace_from_batch(o, 0)
+
+
+def trace_from_batch(o: dict, b: int) -> DinkelbachTrace:
+    st = int(o["status"][b])
+    if st == 3:
+        raise InfeasibleProblemError("inner solver found no feasible allocation at e=0")
+    if st == 4:
+        raise NotImplementedError("non-exclusive seating (products-active families)")
+    tr = DinkelbachTrace()
+    n_it = int(o["outer_iters"][b])
+    for i in range(n_it):
+        stats = SolveStats(rounds=int(o["rounds_trace"][b, i]),
+                           total_sweeps=int(o["sweeps_trace"][b, i]))
+        tr.iterations.append(DinkelbachIteration(e=float(o["e_trace"][b, i]),
+                                                 surplus=float(o["surplus_trace"][b, i]),
+                                                 inner_stats=stats))
+    tr.status = _abi.HCRAN_ST[st]
+    tr.cap_hit = st == 1
+    tr.final_e = float(o["final_e"][b])
+    tr.final_allocation = PowerAllocation(p=o["p"][b].copy(), rho=o["rho"][b].copy(),
+                                          a=o["a"][b].copy())
+    tr.xi = o["xi"][b].copy()
+    tr.zeta = o["zeta"][b].copy()
+    return tr

@@ -1,0 +1,48 @@
+// TEST-ONLY host emulation of the device solver (one CTA of one thread).
+//
+// Compiles paper_1803_07772_b200/csrc/hcran_solver.cuh with the HostEx policy
+// so the CPU test-suite can debug the kernel's logic in the GPU-less build
+// container and compare it with the oracle.  It is never loaded by the
+// product package (which requires the sm_100a library) nor by bench.py.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include "../../paper_1803_07772_b200/csrc/hcran_solver.cuh"
+
+using namespace hcran;
+
+extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in_t* in,
+                               hcran_batch_out_t* out, int mode, int64_t first, int64_t count,
+                               int dense_off) {
+  Work W;
+  size_t bytes = W.layout(nullptr, prob->M, prob->K, prob->N, true);
+  char* base = (char*)aligned_alloc(256, (bytes + 255) & ~size_t(255));
+  if (!base) return -1;
+  memset(base, 0, bytes);
+  W.layout(base, prob->M, prob->K, prob->N, true);
+  View v;
+  v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
+  v.p_max = prob->p_max; v.mask = prob->p_mask; v.eta = prob->eta; v.w = prob->weights;
+  v.sig = prob->sigma; v.static_power = prob->static_power; v.tol = prob->tol;
+  v.B = in->B; v.gamma = in->gamma; v.elastic = in->elastic; v.min_rates = in->min_rates;
+  v.e_fixed = in->e_fixed; v.warm_p = in->warm_p; v.out = *out;
+  v.dense = 0;
+  v.flag_int = nullptr;
+  v.flag_in = nullptr;
+  HostEx ex;
+  Ctl ctl;
+  memset(&ctl, 0, sizeof(ctl));
+  Solver<HostEx> S(ex, v, W, ctl);
+  for (int64_t b = first; b < first + count && b < in->B; ++b) {
+    // pass 1: seated-pair SIC family; pass 2 (floor ties only): dense family
+    for (int pass = 0; pass < 2; ++pass) {
+      v.dense = pass;
+      S.load_instance(b);
+      if (mode == 0) S.dinkelbach(b);
+      else S.fixed_e(b);
+      if (!ctl.fg || dense_off) break;
+    }
+  }
+  free(base);
+  return 0;
+}

@@ -1,0 +1,122 @@
+"""GPU parity: libhcran_b200.so (sm_100a) through the C ABI against the
+reference's golden outputs (tests/golden, produced by the unmodified
+reference) and, at full BASELINE sizes, against size-independent properties.
+
+Bar (BASELINE.json north_star): per-instance EE and total power within 1e-4
+relative, rho/a identical, except on the reference's own near-tie instances
+(golden `near_tie`)."""
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1803_07772_b200 import ScaleSolver, solve, solve_batch  # noqa: E402
+from paper_1803_07772_b200.scenarios import workload_batch, workload_instance  # noqa: E402
+from paper_1803_07772_b200.model import PowerAllocation  # noqa: E402
+
+
+def host(o):
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in o.items()
+            if not k.startswith("_")}
+
+
+def mismatches(g, o, idx):
+    bad = []
+    for j, i in enumerate(idx):
+        if g["near_tie"][i]:
+            continue
+        ok = (o["status"][j] == g["status"][i]
+              and rel(o["ee"][j], g["ee"][i]) <= 1e-4
+              and rel(o["total_power"][j], g["total_power"][i]) <= 1e-4
+              and np.array_equal(o["rho"][j], g["rho"][i])
+              and np.array_equal(o["a"][j], g["a"][i]))
+        if not ok:
+            bad.append((int(i), float(o["ee"][j]), float(g["ee"][i])))
+    return bad
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+def test_dinkelbach_matches_reference(golden, name):
+    g = golden(name)
+    idx = np.arange(len(g["draw"]))
+    b = workload_batch(name, g["draw"][idx])
+    o = host(solve_batch(b.cfg, b.gamma, b.sigma))
+    assert o["launches"] >= 1
+    assert mismatches(g, o, idx) == []
+    assert np.all(o["feasible"][g["feasible"][idx]] == 1)
+
+
+def test_fixed_e_matches_reference(golden):
+    g = golden("c4")
+    idx = np.arange(len(g["draw"]))
+    b = workload_batch("c4", g["draw"][idx])
+    o = host(solve_batch(b.cfg, b.gamma, b.sigma, b.elastic, b.min_rates, mode="fixed_e",
+                         e_fixed=b.e_fixed))
+    for j in idx:
+        assert o["status"][j] == g["status"][j]
+        assert rel(o["objective"][j], g["objective"][j]) <= 1e-4, j
+        assert np.array_equal(o["rho"][j], g["rho"][j]) and np.array_equal(o["a"][j], g["a"][j])
+
+
+def test_device_matches_host_emulation():
+    """Same source compiled for the host (tests/emu): results agree to FMA-level noise."""
+    from emu import runner
+    b = workload_batch("c0", range(32))
+    o = host(solve_batch(b.cfg, b.gamma, b.sigma))
+    e = runner.run(b.cfg, b.gamma, b.sigma, mode=0)
+    agree = np.abs(o["ee"] - e["ee"]) <= 1e-9 * np.abs(e["ee"])
+    assert agree.mean() >= 0.9
+
+
+def test_reference_shaped_api(golden):
+    g = golden("c0")
+    cfg, ch, _ = workload_instance("c0", 3)
+    tr = solve(ch, cfg)
+    assert tr.status == "converged"
+    assert rel(tr.final_e, g["ee"][3]) <= 1e-4
+    es = tr.e_values
+    assert all(b > a for a, b in zip(es, es[1:]))
+    assert np.array_equal(tr.final_allocation.rho, g["rho"][3])
+    res = ScaleSolver().solve_fixed_e(ch, cfg, 0.0)
+    assert res.status == "ok" and res.stats.total_sweeps > 0
+    warm = ScaleSolver().solve_fixed_e(ch, cfg, 5.0, warm_start=res.allocation)
+    assert warm.status == "ok" and warm.stats.used_warm_start
+
+
+@pytest.mark.parametrize("name,count", [("c1", 256), ("c2", 64)])
+def test_full_size_properties(name, count):
+    """Size-independent invariants at BASELINE sizes: feasibility
+    (check_feasibility on device), EE = R/P, one head per user, <= l_max users
+    per (RRH, subcarrier), budgets, rho/a consistent with p."""
+    b = workload_batch(name, range(1000, 1000 + count))
+    o = host(solve_batch(b.cfg, b.gamma, b.sigma))
+    cfg = b.cfg
+    ok = o["status"] <= 2
+    assert ok.mean() >= 0.98
+    assert np.all(o["feasible"][ok] == 1)
+    assert np.allclose(o["ee"][ok], o["sum_rate"][ok] / o["total_power"][ok], rtol=1e-12)
+    p = o["p"][ok]
+    assert np.all(p >= 0) and np.all(p <= cfg.p_mask * (1 + 1e-9))
+    assert np.all(p.sum(axis=(2, 3)) <= cfg.p_max * (1 + 1e-9))
+    assert np.all((p > 0).sum(axis=2) <= cfg.l_max)
+    assert np.all((p.sum(axis=3) > 0).sum(axis=1) <= 1)
+    assert np.all(o["rho"][ok].sum(axis=2) <= cfg.l_max)
+    assert np.all(o["a"][ok].sum(axis=1) <= 1)
+    st = ~cfg.elastic_mask()
+    assert np.all(o["zeta"][ok][:, ~st] == 0)
+
+
+def test_sharding_is_order_free():
+    """Results depend only on the instance (the multi-GPU split never changes them)."""
+    b = workload_batch("c0", range(16))
+    full = host(solve_batch(b.cfg, b.gamma, b.sigma))
+    half = host(solve_batch(b.cfg, b.gamma[8:], b.sigma))
+    assert np.array_equal(full["p"][8:], half["p"])
+    assert np.array_equal(full["ee"][8:], half["ee"])
