@@ -19,6 +19,7 @@ HEADERS = [os.path.join(CSRC, f) for f in ("hcran_solver.cuh", "hcran_exec.cuh",
     [os.path.join(ROOT, "include", "hcran_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+              "--fmad=false",  # the reference rounds every product (numpy): keep cancellations identical
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC", "-lcudart"]
 
 
