@@ -140,6 +140,12 @@ int hcran_b200_solve_fixed_e_batch(const hcran_problem_t* prob, const hcran_batc
                                    hcran_batch_out_t* out, void* workspace,
                                    size_t ws_bytes, void* stream);
 
+/* Which engine the solver picks for this problem: engine 1 = shared-memory
+ * rounds engine on a thread-block cluster of `cluster` CTAs (smem bytes per
+ * CTA), engine 0 = global-workspace engine (shapes whose slices do not fit). */
+int hcran_b200_engine(const hcran_problem_t* prob, int64_t B, int device, int32_t* engine,
+                      int32_t* cluster, size_t* smem);
+
 /* Kernel launches issued by the last successful call on this thread. */
 int32_t hcran_b200_last_launches(void);
 

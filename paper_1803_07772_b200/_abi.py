@@ -65,6 +65,10 @@ def bind_device_lib(lib: C.CDLL) -> C.CDLL:
         fn.argtypes = [C.POINTER(Problem), C.POINTER(BatchIn), C.POINTER(BatchOut),
                        C.c_void_p, C.c_size_t, C.c_void_p]
         fn.restype = C.c_int
+    lib.hcran_b200_engine.argtypes = [C.POINTER(Problem), C.c_int64, C.c_int,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_size_t)]
+    lib.hcran_b200_engine.restype = C.c_int
     lib.hcran_b200_last_launches.argtypes = []
     lib.hcran_b200_last_launches.restype = C.c_int32
     lib.hcran_b200_version.argtypes = []
@@ -73,4 +77,4 @@ def bind_device_lib(lib: C.CDLL) -> C.CDLL:
 
 
 EXPORTED = ("hcran_b200_plan", "hcran_b200_solve_batch", "hcran_b200_solve_fixed_e_batch",
-            "hcran_b200_last_launches", "hcran_b200_version")
+            "hcran_b200_engine", "hcran_b200_last_launches", "hcran_b200_version")

@@ -9,7 +9,8 @@
 // sweeps) is absorbed by the queue.
 #include <cuda_runtime.h>
 #include <stdio.h>
-#include "hcran_solver.cuh"
+#include <stdlib.h>
+#include "hcran_rounds.cuh"
 
 using namespace hcran;
 
@@ -40,6 +41,56 @@ static __global__ void __launch_bounds__(HCRAN_THREADS)
     if (mode == 0) S.dinkelbach(b);
     else S.fixed_e(b);
     __syncthreads();
+  }
+}
+
+// Cluster kernel: the instance's SCA rounds run on a thread-block cluster whose
+// CTAs hold subcarrier slices in shared memory (hcran_rounds.cuh); the leader
+// CTA (rank 0) runs the outer loop, seating and repair on the global workspace.
+#define RE_THREADS 512
+
+static __global__ void __launch_bounds__(RE_THREADS, 1)
+    hcran_cluster_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ double red[2 * RE_THREADS / 32];
+  __shared__ Ctl ctl;
+  __shared__ ReCmd cmd;
+  __shared__ long long next;
+  DevEx ex;
+  ex.init(red);
+  ClusterDev cx;
+  cx.init();
+  ReMem R;
+  R.layout(dsm, v.M, v.K, v.N / cx.csize, v.L, v.N, RE_THREADS / 32);
+  Rounds<DevEx, ClusterDev> RE(ex, cx, v, R);
+  const int cid = blockIdx.x / cx.csize;
+  Work W;
+  W.layout(ws + (size_t)cid * per_cta, v.M, v.K, v.N, false);
+  if (cx.crank == 0) {
+    Solver<DevEx, Rounds<DevEx, ClusterDev>> S(ex, v, W, ctl);
+    S.re = &RE;
+    S.re_cmd = &cmd;
+    for (;;) {
+      if (threadIdx.x == 0) next = (long long)atomicAdd(counter, 1);
+      __syncthreads();
+      const long long b = next;
+      __syncthreads();
+      if (b >= v.B) break;
+      S.load_instance(b);
+      if (mode == 0) S.dinkelbach(b);
+      else S.fixed_e(b);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cmd.op = 0;
+    __threadfence();
+    cx.csync();
+  } else {
+    for (;;) {
+      cx.csync();
+      const ReCmd c = *cx.remote(&cmd, 0);
+      if (c.op == 0) break;
+      RE.run(c, W.p);
+    }
   }
 }
 
@@ -83,16 +134,92 @@ static int resident_ctas(int device) {
   return sms * per_sm;
 }
 
+static size_t re_smem(const hcran_problem_t* p, int cs) {
+  ReMem r;
+  return r.layout(nullptr, p->M, p->K, p->N / cs, p->l_max, p->N, RE_THREADS / 32);
+}
+
+struct Plan {
+  int engine;        // 1: cluster rounds engine, 0: global-workspace engine
+  int cs;            // cluster size
+  int64_t grid;      // CTAs of pass 1
+  int64_t slots;     // pass-1 workspace slots (clusters or CTAs)
+  size_t per, smem;  // bytes per slot / dynamic smem per CTA
+  int64_t grid2;     // CTAs of pass 2 (dense SIC family)
+  size_t perd;
+  size_t total;
+};
+
+static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P) {
+  const int64_t Bp = B > 0 ? B : 1;
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (maxsm <= 0) maxsm = 232448;
+  const size_t budget = (size_t)maxsm - 2048;  // static shared memory of the kernel
+  int cs = 0;
+  const char* force = getenv("HCRAN_CLUSTER");
+  const int want = force ? atoi(force) : 0;
+  for (int c = 1; c <= 16; c <<= 1) {
+    if (prob->N % c) continue;
+    if (want > 0 && c != want) continue;
+    if (want < 0) break;  // HCRAN_CLUSTER=-1: force the global engine
+    if (re_smem(prob, c) <= budget) { cs = c; break; }
+  }
+  P->perd = per_cta_bytes(prob, true);
+  if (cs > 0) {
+    P->engine = 1;
+    P->cs = cs;
+    P->smem = re_smem(prob, cs);
+    P->per = per_cta_bytes(prob);
+    cudaFuncSetAttribute(hcran_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)P->smem);
+    if (cs > 8) cudaFuncSetAttribute(hcran_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * 64);
+    cfg.blockDim = dim3(RE_THREADS);
+    cfg.dynamicSmemBytes = P->smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, hcran_cluster_kernel, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      ncl = sms / cs;
+    }
+    int64_t nc = ncl;
+    if (nc > Bp) nc = Bp;
+    P->slots = nc;
+    P->grid = nc * cs;
+  } else {
+    P->engine = 0;
+    P->cs = 1;
+    P->smem = 0;
+    P->per = per_cta_bytes(prob);
+    int64_t g = resident_ctas(device);
+    if (g > Bp) g = Bp;
+    P->slots = g;
+    P->grid = g;
+  }
+  P->grid2 = dense_ctas(prob, Bp, P->grid);
+  P->total = HEADER + flags_bytes(Bp) + (size_t)P->slots * P->per + (size_t)P->grid2 * P->perd;
+  return HCRAN_OK;
+}
+
 extern "C" int hcran_b200_plan(const hcran_problem_t* prob, int64_t B, int device,
                                int32_t* grid_out, size_t* ws_bytes_out) {
   int rc = check_problem(prob);
   if (rc) return rc;
   if (B < 0 || !grid_out || !ws_bytes_out) return HCRAN_E_ARG;
-  int64_t grid = resident_ctas(device);
-  if (B < grid) grid = B > 0 ? B : 1;
-  *grid_out = (int32_t)grid;
-  *ws_bytes_out = HEADER + flags_bytes(B) + (size_t)grid * per_cta_bytes(prob) +
-                  (size_t)dense_ctas(prob, B, grid) * per_cta_bytes(prob, true);
+  Plan P;
+  make_plan(prob, B, device, &P);
+  *grid_out = (int32_t)P.grid;
+  *ws_bytes_out = P.total;
   return HCRAN_OK;
 }
 
@@ -106,14 +233,9 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   if (in->B <= 0) return HCRAN_OK;
   int device = 0;
   cudaGetDevice(&device);
-  const size_t per = per_cta_bytes(prob), perd = per_cta_bytes(prob, true);
-  int64_t grid = resident_ctas(device);
-  if (in->B < grid) grid = in->B;
-  const int64_t grid2 = dense_ctas(prob, in->B, grid);
-  const size_t fixed = HEADER + flags_bytes(in->B) + (size_t)grid2 * perd;
-  if (ws_bytes < fixed + per) return HCRAN_E_WORKSPACE;
-  const int64_t fit = (int64_t)((ws_bytes - fixed) / per);
-  if (fit < grid) grid = fit;
+  Plan P;
+  make_plan(prob, in->B, device, &P);
+  if (ws_bytes < P.total) return HCRAN_E_WORKSPACE;
   View v;
   v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
   v.p_max = prob->p_max; v.mask = prob->p_mask; v.eta = prob->eta; v.w = prob->weights;
@@ -124,16 +246,47 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   char* base = (char*)workspace;
   uint8_t* flags = (uint8_t*)(base + HEADER);
   char* slots1 = base + HEADER + flags_bytes(in->B);
-  char* slots2 = slots1 + (size_t)grid * per;
+  char* slots2 = slots1 + (size_t)P.slots * P.per;
   if (cudaMemsetAsync(base, 0, HEADER, s) != cudaSuccess) return HCRAN_E_LAUNCH;
   v.dense = 0; v.flag_int = flags; v.flag_in = nullptr;
-  hcran_solve_kernel<<<(unsigned)grid, HCRAN_THREADS, 0, s>>>(v, slots1, per, (int*)base, mode);
+  if (P.engine == 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)P.grid);
+    cfg.blockDim = dim3(RE_THREADS);
+    cfg.dynamicSmemBytes = P.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, hcran_cluster_kernel, v, slots1, P.per, (int*)base, mode) !=
+        cudaSuccess)
+      return HCRAN_E_LAUNCH;
+  } else {
+    hcran_solve_kernel<<<(unsigned)P.grid, HCRAN_THREADS, 0, s>>>(v, slots1, P.per, (int*)base,
+                                                                  mode);
+  }
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   v.dense = 1; v.flag_int = nullptr; v.flag_in = flags;
-  hcran_solve_kernel<<<(unsigned)grid2, HCRAN_THREADS, 0, s>>>(v, slots2, perd, (int*)base + 1,
-                                                               mode);
+  hcran_solve_kernel<<<(unsigned)P.grid2, HCRAN_THREADS, 0, s>>>(v, slots2, P.perd, (int*)base + 1,
+                                                                 mode);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   g_last_launches = 2;
+  return HCRAN_OK;
+}
+
+extern "C" int hcran_b200_engine(const hcran_problem_t* prob, int64_t B, int device,
+                                 int32_t* engine, int32_t* cluster, size_t* smem) {
+  int rc = check_problem(prob);
+  if (rc) return rc;
+  Plan P;
+  make_plan(prob, B, device, &P);
+  if (engine) *engine = P.engine;
+  if (cluster) *cluster = P.cs;
+  if (smem) *smem = P.smem;
   return HCRAN_OK;
 }
 

@@ -7,13 +7,13 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
-#include "../../paper_1803_07772_b200/csrc/hcran_solver.cuh"
+#include "../../paper_1803_07772_b200/csrc/hcran_rounds.cuh"
 
 using namespace hcran;
 
 extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in_t* in,
                                hcran_batch_out_t* out, int mode, int64_t first, int64_t count,
-                               int dense_off) {
+                               int dense_off, int use_engine) {
   Work W;
   size_t bytes = W.layout(nullptr, prob->M, prob->K, prob->N, true);
   char* base = (char*)aligned_alloc(256, (bytes + 255) & ~size_t(255));
@@ -32,7 +32,21 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   HostEx ex;
   Ctl ctl;
   memset(&ctl, 0, sizeof(ctl));
-  Solver<HostEx> S(ex, v, W, ctl);
+  // shared-memory rounds engine with a one-CTA "cluster"
+  ReMem R;
+  size_t rbytes = R.layout(nullptr, prob->M, prob->K, prob->N, prob->l_max, prob->N, 1);
+  char* rbase = (char*)aligned_alloc(256, (rbytes + 255) & ~size_t(255));
+  memset(rbase, 0, rbytes);
+  R.layout(rbase, prob->M, prob->K, prob->N, prob->l_max, prob->N, 1);
+  ClusterHost cx;
+  Rounds<HostEx, ClusterHost> RE(ex, cx, v, R);
+  ReCmd cmd;
+  memset(&cmd, 0, sizeof(cmd));
+  Solver<HostEx, Rounds<HostEx, ClusterHost>> S(ex, v, W, ctl);
+  if (use_engine) {
+    S.re = &RE;
+    S.re_cmd = &cmd;
+  }
   for (int64_t b = first; b < first + count && b < in->B; ++b) {
     // pass 1: seated-pair SIC family; pass 2 (floor ties only): dense family
     for (int pass = 0; pass < 2; ++pass) {
@@ -44,5 +58,6 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
     }
   }
   free(base);
+  free(rbase);
   return 0;
 }

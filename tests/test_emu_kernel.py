@@ -26,12 +26,13 @@ def _check_dinkelbach(g, out, idx):
     return bad
 
 
+@pytest.mark.parametrize("engine", [True, False], ids=["smem-engine", "global-engine"])
 @pytest.mark.parametrize("name", ["c0", "c1"])
-def test_emu_dinkelbach_golden(golden, name):
+def test_emu_dinkelbach_golden(golden, name, engine):
     g = golden(name)
     idx = np.arange(len(g["draw"]))
     b = workload_batch(name, g["draw"][idx])
-    out = runner.run(b.cfg, b.gamma, b.sigma, mode=0)
+    out = runner.run(b.cfg, b.gamma, b.sigma, mode=0, engine=engine)
     assert _check_dinkelbach(g, out, idx) == []
     assert np.all(out["feasible"][g["feasible"][idx]] == 1)
     # iteration counts follow the reference's trajectory
@@ -39,12 +40,13 @@ def test_emu_dinkelbach_golden(golden, name):
     assert np.mean(out["outer_iters"] == n_ref) >= 0.95
 
 
-def test_emu_fixed_e_golden(golden):
+@pytest.mark.parametrize("engine", [True, False], ids=["smem-engine", "global-engine"])
+def test_emu_fixed_e_golden(golden, engine):
     g = golden("c4")
     idx = np.arange(len(g["draw"]))
     b = workload_batch("c4", g["draw"][idx])
     out = runner.run(b.cfg, b.gamma, b.sigma, mode=1, elastic=b.elastic, min_rates=b.min_rates,
-                     e_fixed=b.e_fixed)
+                     e_fixed=b.e_fixed, engine=engine)
     for j in idx:
         assert out["status"][j] == g["status"][j]
         assert rel(out["objective"][j], g["objective"][j]) <= 1e-4, j
