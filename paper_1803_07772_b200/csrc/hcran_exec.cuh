@@ -40,6 +40,10 @@ struct DevEx {
   __device__ __forceinline__ void sync() const { __syncthreads(); }
   __device__ __forceinline__ void wsync() const { __syncwarp(); }
   __device__ __forceinline__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
+  // named barrier over `count` threads (a warp group); id 1..15
+  __device__ __forceinline__ void named_sync(int id, int count) const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
   // warp-level (all lanes receive the result; fixed butterfly order)
   __device__ __forceinline__ double wsum(double v) const {
 #pragma unroll
@@ -85,6 +89,7 @@ struct HostEx {
   void sync() const {}
   void wsync() const {}
   bool any(bool p) const { return p; }
+  void named_sync(int, int) const {}
   double wsum(double v) const { return v; }
   double wmax(double v) const { return v; }
   int wmaxi(int v) const { return v; }

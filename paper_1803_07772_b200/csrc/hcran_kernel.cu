@@ -17,8 +17,11 @@ using namespace hcran;
 #ifndef HCRAN_THREADS
 #define HCRAN_THREADS 256
 #endif
+#ifndef HCRAN_MINB
+#define HCRAN_MINB 1
+#endif
 
-static __global__ void __launch_bounds__(HCRAN_THREADS)
+static __global__ void __launch_bounds__(HCRAN_THREADS, HCRAN_MINB)
     hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
   // pass 1 (v.dense == 0): every instance, seated-pair SIC family, flags floor ties.
   // pass 2 (v.dense == 1): only instances flagged by pass 1, dense pair family.
@@ -83,12 +86,16 @@ static __global__ void __launch_bounds__(RE_THREADS, 1)
     }
     if (threadIdx.x == 0) cmd.op = 0;
     __threadfence();
-    cx.csync();
+    cx.csync();  // publish EXIT
+    cx.csync();  // keep this CTA's shared memory alive until every follower has read it
   } else {
     for (;;) {
       cx.csync();
       const ReCmd c = *cx.remote(&cmd, 0);
-      if (c.op == 0) break;
+      if (c.op == 0) {
+        cx.csync();
+        break;
+      }
       RE.run(c, W.p);
     }
   }
@@ -130,7 +137,7 @@ static int resident_ctas(int device) {
           cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  if (per_sm > 4) per_sm = 4;  // state lives in the workspace: bound its footprint
+  if (per_sm > 8) per_sm = 8;  // state lives in the workspace: bound its footprint
   return sms * per_sm;
 }
 
@@ -158,7 +165,7 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
   const size_t budget = (size_t)maxsm - 2048;  // static shared memory of the kernel
   int cs = 0;
   const char* force = getenv("HCRAN_CLUSTER");
-  const int want = force ? atoi(force) : 0;
+  const int want = force ? atoi(force) : -1;  // default: global-workspace engine (faster)
   for (int c = 1; c <= 16; c <<= 1) {
     if (prob->N % c) continue;
     if (want > 0 && c != want) continue;
@@ -303,6 +310,23 @@ extern "C" int hcran_b200_solve_fixed_e_batch(const hcran_problem_t* prob,
 }
 
 extern "C" int32_t hcran_b200_last_launches(void) { return g_last_launches; }
+
+// phase profiler readout (only meaningful in a -DHCRAN_PROFILE build)
+extern "C" int hcran_b200_phase_cycles(unsigned long long* out32, int reset) {
+#if defined(HCRAN_PROFILE)
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+#else
+  for (int i = 0; i < 32; ++i) out32[i] = 0;
+  (void)reset;
+  return -1;
+#endif
+}
 
 extern "C" const char* hcran_b200_version(void) {
   return "hcran_b200 0.1.0 (abi 1, sm_100a, fp64 core)";

@@ -26,7 +26,7 @@ from . import _abi, pack
 from .model import PowerAllocation
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhcran_b200.so")
+LIB_PATH = os.environ.get("HCRAN_LIB", os.path.join(_HERE, "libhcran_b200.so"))
 
 
 class InfeasibleProblemError(RuntimeError):

@@ -1,0 +1,30 @@
+"""Build a -DHCRAN_PROFILE copy of the library and print per-phase cycle shares."""
+import ctypes as C, os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1803_07772_b200 import build as B, solver
+lib_path = os.path.join(ROOT, 'tools', 'libhcran_prof.so')
+if not os.path.exists(lib_path):
+    cmd = [B.nvcc()] + B.NVCC_FLAGS + ['-DHCRAN_PROFILE', '-I' + os.path.join(ROOT, 'include'), '-o', lib_path] + B.SOURCES
+    subprocess.run(cmd, check=True, capture_output=True)
+solver.LIB_PATH = lib_path
+lib = solver.library()
+lib.hcran_b200_phase_cycles.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+from paper_1803_07772_b200 import solve_batch
+from paper_1803_07772_b200.scenarios import workload_batch
+name = sys.argv[1] if len(sys.argv) > 1 else 'c1'
+nb = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+b = workload_batch(name, range(nb))
+out = (C.c_ulonglong * 32)()
+solve_batch(b.cfg, b.gamma, b.sigma)
+lib.hcran_b200_phase_cycles(out, 1)
+o = solve_batch(b.cfg, b.gamma, b.sigma)
+lib.hcran_b200_phase_cycles(out, 0)
+names = {0: 'sw:totals+full', 1: 'sw:decode pass', 2: 'sw:utot', 3: 'sw:psi_cross+pairs', 4: 'sw:num/den', 5: 'sw:X1 partials+exchange',
+         6: 'sw:bisection', 7: 'sw:closed form', 8: 'sw:X3 exchange', 10: 'round_start', 11: 'round_end', 12: 'run:build_seats',
+         16: 'inner:setup', 17: 'inner:rounds', 18: 'inner:repair', 19: 'inner:feasible'}
+tot = sum(out[i] for i in range(0, 9))
+print('sweeps', int(o['sweeps'].sum().item()), 'instances', nb)
+for i in range(32):
+    if out[i]:
+        print(f"{names.get(i, i):28s} {out[i]/1e9:9.3f} Gcyc  {100*out[i]/max(tot,1):6.1f}% of sweep")
