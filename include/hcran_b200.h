@@ -81,7 +81,19 @@ typedef struct hcran_problem {
   const double* sigma;    /* [M][K][N]  noise power, W                        */
   double static_power;    /* fibre + circuit floor, W (model.py:173-176)      */
   hcran_tolerances_t tol;
+  int32_t sic_mode;       /* HCRAN_SIC_SEATED (default), _DENSE or _SEATED_FAST */
 } hcran_problem_t;
+
+/* SIC multiplier family (scale.py:668-723, 776-819).  DENSE tracks a
+ * multiplier for every oriented user pair on every (RRH, subcarrier), exactly
+ * as the reference.  SEATED tracks the pairs whose members are both seated and
+ * re-solves with DENSE any instance in which a seat's numerator vanishes while
+ * its denominator is not positive (a "floor tie": the
+ * reference then decides the seat from the floor-level (~1e-75) multipliers of
+ * unseated pairs); ~7x faster than DENSE at config[1]. */
+#define HCRAN_SIC_SEATED 0      /* default: exact on every golden draw        */
+#define HCRAN_SIC_DENSE 1       /* dense family for every inner solve                     */
+#define HCRAN_SIC_SEATED_FAST 2 /* seated family, floor ties NOT re-run (opt-in, inexact) */
 
 /* Per-instance inputs. */
 typedef struct hcran_batch_in {
@@ -119,8 +131,8 @@ typedef struct hcran_batch_out {
   double* work;          /* [B] algorithmic FP64 work, flop-equivalents */
 } hcran_batch_out_t;
 
-/* flags: a seat met num == den == 0 in the seated-pair SIC model, i.e. the
- * reference would decide it from floor-level multipliers of unseated pairs
+/* flags: a seat met num == 0 with den <= 0 in the seated-pair SIC model, i.e.
+ * the reference would decide it from floor-level multipliers of unseated pairs
  * (the instance is re-solved with the dense pair family). */
 #define HCRAN_FLAG_FLOOR_TIE 1
 #define HCRAN_FLAG_DENSE_RESOLVED 2 /* result comes from the dense-pair re-solve */

@@ -203,8 +203,16 @@ class Ctx:
     GAINS = (0.6, 0.8, 0.6, 0.6, 0.6)   # scale.py:495 (budget, rate, pair, tuple, sic)
     RATE_SCALE = 10.0                    # scale.py:689
 
-    def __init__(self, P: Prob, e: float):
+    def __init__(self, P: Prob, e: float, sic: str = "dense"):
+        """sic="dense": the reference's SIC family over every oriented pair.
+        sic="seated": the device's default model, multipliers only on pairs
+        whose members are both seated (the family is re-created per seating);
+        `floor_tie` records a seat whose numerator vanishes exactly while its
+        denominator is not positive -- the reference then decides the seat from
+        the floor-level multipliers of unseated pairs."""
         self.P, self.e = P, float(e)
+        self.sic = sic
+        self.floor_tie = False
         M, K, N = P.shape
         self.p_floor = 1e-30 * P.max_mask
         iu, ju = np.triu_indices(K, 1)
@@ -415,6 +423,7 @@ class InnerStats:
     status: str = "ok"
     infeasible_reason: str | None = None
     true_objective: float = float("nan")
+    floor_tie: bool = False
 
 
 def sca_rounds(ctx: Ctx, p0: np.ndarray, stats: InnerStats):
@@ -423,6 +432,9 @@ def sca_rounds(ctx: Ctx, p0: np.ndarray, stats: InnerStats):
     seat = p0 > ctx.p_floor
     if not seating_exclusive(seat, P.l_max):
         raise ProductsActive("non-exclusive seating")
+    pair_mask = None
+    if ctx.sic == "seated":
+        pair_mask = ctx.take(seat, ctx.s_idx) & ctx.take(seat, ctx.w_idx)
     mask_eff = np.where(seat, P.p_mask, ctx.p_floor)
     zeta = np.where(P.elastic, 0.0, 1.0)
     zt = np.zeros_like(ctx.g_s)
@@ -437,11 +449,15 @@ def sca_rounds(ctx: Ctx, p0: np.ndarray, stats: InnerStats):
         p_round = p
         for v in range(1, tol.v_max + 1):
             num, den, rate_slack, sic_slack = ctx.analyze(p, zeta, zt, alpha, beta, lin)
+            if pair_mask is not None and np.any(seat & (num == 0.0) & ~(den > 0.0)):
+                ctx.floor_tie = True
             xi = budget_multiplier(num, den, mask_eff, P.p_max, xi)
             p_next = clamp_update(num, den + xi[:, None, None], mask_eff, ctx.p_floor)
             damp = 1.0 / math.sqrt(max(v, 1))
             zeta = np.clip(zeta + damp * ctx.zeta_step * rate_slack, 0.0, ctx.zeta_cap)
             zt = np.clip(zt + damp * ctx.sic_step * sic_slack, 0.0, ctx.sic_cap)
+            if pair_mask is not None:
+                zt = np.where(pair_mask, zt, 0.0)
             delta = np.abs(p_next - p).max(axis=(1, 2))
             p = p_next
             stats.total_sweeps += 1
@@ -693,8 +709,18 @@ class InnerResult:
     stats: InnerStats
 
 
-def solve_fixed_e(P: Prob, e: float, warm_p: np.ndarray | None = None) -> InnerResult:
-    ctx = Ctx(P, e)
+def solve_fixed_e(P: Prob, e: float, warm_p: np.ndarray | None = None,
+                  sic: str = "dense") -> InnerResult:
+    """sic="device": the B200 default -- the seated-pair SIC model, with the
+    inner solve redone from its start with the dense family when it met a
+    floor tie (a seat with num == 0 and den <= 0)."""
+    if sic == "device":
+        res = solve_fixed_e(P, e, warm_p, "seated")
+        if res.stats.floor_tie:
+            res = solve_fixed_e(P, e, warm_p, "dense")
+            res.stats.floor_tie = True
+        return res
+    ctx = Ctx(P, e, sic)
     stats = InnerStats()
     if warm_p is not None:
         p0 = np.clip(warm_p, ctx.p_floor, P.p_mask)
@@ -718,6 +744,7 @@ def solve_fixed_e(P: Prob, e: float, warm_p: np.ndarray | None = None) -> InnerR
         return InnerResult(q, None, None, "infeasible", stats)
     rho, a = indicators(P, q)
     stats.true_objective = true_objective(P, q, e)
+    stats.floor_tie = ctx.floor_tie
     return InnerResult(q, rho, a, "ok", stats)
 
 
@@ -731,15 +758,20 @@ class Trace:
     rho: np.ndarray | None = None
     a: np.ndarray | None = None
     status: str = "converged"
+    floor_tie: bool = False
 
 
-def dinkelbach(P: Prob, e0: float = 0.0) -> Trace:
+def dinkelbach(P: Prob, e0: float = 0.0, sic: str = "dense") -> Trace:
+    """sic="dense": the reference.  sic="device": the B200 default path
+    (see solve_fixed_e)."""
     tol = P.tol
     tr = Trace()
     e = e0
     warm = None
     for _ in range(tol.outer_max):
-        res = solve_fixed_e(P, e, warm.p if warm is not None else None)
+        res = solve_fixed_e(P, e, warm.p if warm is not None else None, sic)
+        if getattr(res.stats, "floor_tie", False):
+            tr.floor_tie = True
         if res.status != "ok":
             if warm is None:
                 raise Infeasible(res.stats.infeasible_reason)

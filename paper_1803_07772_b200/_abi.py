@@ -26,7 +26,7 @@ class Problem(C.Structure):
     _fields_ = [("M", C.c_int32), ("K", C.c_int32), ("N", C.c_int32), ("l_max", C.c_int32),
                 ("p_max", C.c_void_p), ("p_mask", C.c_void_p), ("eta", C.c_void_p),
                 ("weights", C.c_void_p), ("sigma", C.c_void_p),
-                ("static_power", C.c_double), ("tol", Tolerances)]
+                ("static_power", C.c_double), ("tol", Tolerances), ("sic_mode", C.c_int32)]
 
 
 class BatchIn(C.Structure):

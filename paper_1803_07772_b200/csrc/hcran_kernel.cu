@@ -31,7 +31,7 @@ static __global__ void __launch_bounds__(HCRAN_THREADS, HCRAN_MINB)
   DevEx ex;
   ex.init(red);
   Work W;
-  W.layout(ws + (size_t)blockIdx.x * per_cta, v.M, v.K, v.N, v.dense != 0);
+  W.layout(ws + (size_t)blockIdx.x * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0);
   Solver<DevEx> S(ex, v, W, ctl);
   for (;;) {
     if (threadIdx.x == 0) next = (long long)atomicAdd(counter, 1);
@@ -109,6 +109,7 @@ static int check_problem(const hcran_problem_t* p) {
   if (p->M < 1 || p->K < 1 || p->N < 1) return HCRAN_E_SIZE;
   if (p->K > 255 || p->N > 256 || p->M > 31) return HCRAN_E_SIZE;
   if (p->l_max < 1 || p->l_max > SMAX) return HCRAN_E_SIZE;
+  if (p->sic_mode < HCRAN_SIC_SEATED || p->sic_mode > HCRAN_SIC_SEATED_FAST) return HCRAN_E_ARG;
   if (!p->p_max || !p->p_mask || !p->eta || !p->weights || !p->sigma) return HCRAN_E_ARG;
   return HCRAN_OK;
 }
@@ -155,6 +156,8 @@ struct Plan {
   int64_t grid2;     // CTAs of pass 2 (dense SIC family)
   size_t perd;
   size_t total;
+  int dense_all;     // 1: every instance runs the dense SIC pair family in pass 1
+  int dense_ok;      // 1: pass-1 slots carry the dense family (floor ties re-run in place)
 };
 
 static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P) {
@@ -173,6 +176,11 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
     if (re_smem(prob, c) <= budget) { cs = c; break; }
   }
   P->perd = per_cta_bytes(prob, true);
+  P->dense_ok = 0;
+  const char* dn = getenv("HCRAN_DENSE");
+  P->dense_all = prob->sic_mode == HCRAN_SIC_DENSE ? 1 : 0;
+  if (dn) P->dense_all = atoi(dn);
+  if (P->dense_all) cs = 0;
   if (cs > 0) {
     P->engine = 1;
     P->cs = cs;
@@ -207,13 +215,17 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
     P->engine = 0;
     P->cs = 1;
     P->smem = 0;
-    P->per = per_cta_bytes(prob);
     int64_t g = resident_ctas(device);
     if (g > Bp) g = Bp;
     P->slots = g;
     P->grid = g;
+    // floor ties are re-run in place when every slot can carry the dense family
+    P->dense_ok = (!P->dense_all && prob->sic_mode != HCRAN_SIC_SEATED_FAST &&
+                   (size_t)g * P->perd <= ((size_t)24 << 30)) ? 1 : 0;
+    P->per = per_cta_bytes(prob, P->dense_all != 0 || P->dense_ok != 0);
   }
-  P->grid2 = dense_ctas(prob, Bp, P->grid);
+  P->grid2 = (P->dense_all || P->dense_ok || prob->sic_mode == HCRAN_SIC_SEATED_FAST)
+                 ? 0 : dense_ctas(prob, Bp, P->grid);
   P->total = HEADER + flags_bytes(Bp) + (size_t)P->slots * P->per + (size_t)P->grid2 * P->perd;
   return HCRAN_OK;
 }
@@ -255,7 +267,7 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   char* slots1 = base + HEADER + flags_bytes(in->B);
   char* slots2 = slots1 + (size_t)P.slots * P.per;
   if (cudaMemsetAsync(base, 0, HEADER, s) != cudaSuccess) return HCRAN_E_LAUNCH;
-  v.dense = 0; v.flag_int = flags; v.flag_in = nullptr;
+  v.dense = P.dense_all ? 1 : 0; v.dense_ok = P.dense_ok; v.flag_int = flags; v.flag_in = nullptr;
   if (P.engine == 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)P.grid);
@@ -277,7 +289,11 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
                                                                   mode);
   }
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
-  v.dense = 1; v.flag_int = nullptr; v.flag_in = flags;
+  if (P.grid2 == 0) {  // pass 1 already settled every floor tie (or the fast model ignores them)
+    g_last_launches = 1;
+    return HCRAN_OK;
+  }
+  v.dense = 1; v.dense_ok = 0; v.flag_int = nullptr; v.flag_in = flags;
   hcran_solve_kernel<<<(unsigned)P.grid2, HCRAN_THREADS, 0, s>>>(v, slots2, P.perd, (int*)base + 1,
                                                                  mode);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;

@@ -663,7 +663,7 @@ struct Rounds {
         s_den_[s] = base + s_psis_[s] + pc + ((s_dsA_[s] + s_dsB_[s]) + dcr);
         double z = p_[c] * g_[c] * s_inv_[s];
         s_rhat_[s] = s_beta_[s] + al_[c] * log2(fmax(z, ZF));
-        if (s_num_[s] == 0.0 && s_den_[s] == 0.0) flag = true;
+        if (s_num_[s] == 0.0 && !(s_den_[s] > 0.0)) flag = true;  // floor tie
       }
       for (int q = 0; q < npr_[col]; ++q) {
         int pq = col * NPL + q;

@@ -48,7 +48,8 @@ struct Work {
   int32_t* perm;                     // [N]
   // dense SIC pair family (exact mode for floor-tie instances) -- bound when dense
   double *cx, *cxl, *dA, *dB, *nS, *nW, *dg, *ag;  // [C]
-  double *pd_zt, *pd_step;                         // [MN * K(K-1)/2]
+  double *pd_zt, *pd_step;                         // [K(K-1)/2][MN] (pair-major)
+  uint8_t *pq_i, *pq_j;                            // [K(K-1)/2] members of pair q
 
   HD static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -92,8 +93,10 @@ struct Work {
       HC_D(cx, C); HC_D(cxl, C); HC_D(dA, C); HC_D(dB, C); HC_D(nS, C); HC_D(nW, C);
       HC_D(dg, C); HC_D(ag, C);
       HC_D(pd_zt, PD); HC_D(pd_step, PD);
+      HC_B(pq_i, PD / MN + 1); HC_B(pq_j, PD / MN + 1);
     } else {
       cx = cxl = dA = dB = nS = nW = dg = ag = pd_zt = pd_step = nullptr;
+      pq_i = pq_j = nullptr;
     }
 #undef HC_D
 #undef HC_B

@@ -35,11 +35,14 @@ def problem_arrays(cfg, sigma: np.ndarray) -> dict:
             "sigma": sig}
 
 
-def problem_struct(cfg, ptrs: dict) -> _abi.Problem:
+def problem_struct(cfg, ptrs: dict, exact=False) -> _abi.Problem:
+    """exact: False -> HCRAN_SIC_SEATED (default), True -> HCRAN_SIC_DENSE,
+    "fast" -> HCRAN_SIC_SEATED_FAST."""
     return _abi.Problem(M=cfg.n_rrh, K=cfg.n_users, N=cfg.n_subcarriers, l_max=cfg.l_max,
                         p_max=ptrs["p_max"], p_mask=ptrs["p_mask"], eta=ptrs["eta"],
                         weights=ptrs["weights"], sigma=ptrs["sigma"],
-                        static_power=float(cfg.static_power()), tol=tolerances(cfg))
+                        static_power=float(cfg.static_power()), tol=tolerances(cfg),
+                        sic_mode=2 if exact == "fast" else (1 if exact else 0))
 
 
 def instance_arrays(cfgs_or_cfg, gamma: np.ndarray, elastic=None, min_rates=None,

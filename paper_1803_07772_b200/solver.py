@@ -62,17 +62,18 @@ _TORCH_DT = {"f8": "float64", "u1": "uint8", "i4": "int32", "i1": "int8"}
 class _DeviceProblem:
     """Batch-constant config arrays resident on the device + the C struct."""
 
-    def __init__(self, cfg, sigma, device):
+    def __init__(self, cfg, sigma, device, exact=False):
         torch = _torch()
         arrs = pack.problem_arrays(cfg, sigma)
-        self.t = {k: torch.from_numpy(v).to(device) for k, v in arrs.items()}
-        self.struct = pack.problem_struct(cfg, {k: v.data_ptr() for k, v in self.t.items()})
+        self.t = {k: torch.from_numpy(np.array(v)).to(device) for k, v in arrs.items()}
+        self.struct = pack.problem_struct(cfg, {k: v.data_ptr() for k, v in self.t.items()},
+                                          exact=exact)
         self.shape = (cfg.n_rrh, cfg.n_users, cfg.n_subcarriers)
 
 
 def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="dinkelbach",
                 e_fixed=None, warm_p=None, stream=None, outputs=None, device=None,
-                workspace=None, sync=True):
+                workspace=None, sync=True, exact=False):
     """Solve every instance of a batch on the device.
 
     cfg        template NetworkConfig (p_max, p_mask, eta, weights, l_max, tolerances)
@@ -80,6 +81,10 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
     sigma      (M, K, N) noise powers (default: the config's flat noise floor)
     elastic    (B, K) bool / min_rates (B, K): per-instance user classes (default: cfg's)
     mode       "dinkelbach" (full solve) or "fixed_e" (one inner solve per instance)
+    exact      False (default): seated SIC family, inner solves that meet a floor tie
+               are redone with the dense family (HCRAN_SIC_SEATED); True: dense family
+               everywhere (HCRAN_SIC_DENSE); "fast": seated family only, floor ties not
+               redone (HCRAN_SIC_SEATED_FAST, ~3% of config[1] draws then differ)
     outputs    subset of _abi.OUT_FIELDS names to produce (default: all)
     Returns a dict of CUDA tensors keyed like hcran_batch_out_t (plus "launches").
     """
@@ -89,7 +94,7 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
     M, K, N = cfg.n_rrh, cfg.n_users, cfg.n_subcarriers
     if sigma is None:
         sigma = np.full((M, K, N), cfg.noise_density * cfg.subcarrier_bandwidth)
-    prob = _DeviceProblem(cfg, sigma, dev)
+    prob = _DeviceProblem(cfg, sigma, dev, exact=exact)
     if isinstance(gamma, np.ndarray):
         g = torch.from_numpy(np.ascontiguousarray(gamma, np.float64)).to(dev)
     else:

@@ -11,7 +11,6 @@ for p in (ROOT, HERE):
         sys.path.insert(0, p)
 
 GOLDEN = os.path.join(HERE, "golden")
-GOLDEN_FILES = {"c0": "c0_0_128.npz", "c1": "c1_0_24.npz", "c2": "c2_0_7.npz", "c4": "c4_0_256.npz"}
 
 
 def pytest_configure(config):
@@ -19,13 +18,48 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running checks")
 
 
+def _golden_files(name):
+    import glob
+    fs = [f for f in glob.glob(os.path.join(GOLDEN, f"{name}_*_*.npz")) if "_devmodel" not in f]
+    return sorted(fs, key=lambda f: int(os.path.basename(f).split("_")[1]))
+
+
+def _concat(parts):
+    out = {}
+    for k in parts[0]:
+        arrs = [np.asarray(p[k]) for p in parts]
+        if arrs[0].ndim == 0:
+            out[k] = arrs[0]
+            continue
+        if arrs[0].ndim == 2 and k in ("e_values", "surplus", "rounds", "sweeps"):
+            w = max(a.shape[1] for a in arrs)
+            arrs = [np.pad(a, ((0, 0), (0, w - a.shape[1])), constant_values=np.nan) for a in arrs]
+        out[k] = np.concatenate(arrs)
+    return out
+
+
 def load_golden(name):
-    return dict(np.load(os.path.join(GOLDEN, GOLDEN_FILES[name])))
+    """Reference outputs (tests/golden/make_golden.py) of every draw file of a config."""
+    return _concat([dict(np.load(f)) for f in _golden_files(name)])
+
+
+def load_devmodel(name):
+    """Oracle restatement of the B200 default SIC model for the same draws
+    (tests/golden/make_device_model.py); None when not generated."""
+    fs = [f.replace(".npz", "_devmodel.npz") for f in _golden_files(name)]
+    if not all(os.path.exists(f) for f in fs):
+        return None
+    return _concat([dict(np.load(f)) for f in fs])
 
 
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+@pytest.fixture(scope="session")
+def devmodel():
+    return load_devmodel
 
 
 def rel(a, b):

@@ -47,15 +47,14 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
     S.re = &RE;
     S.re_cmd = &cmd;
   }
+  // seated-pair SIC family with floor ties re-run dense in place (dense_off: no
+  // re-run, to expose the seated model); HCRAN_SIC_DENSE: dense everywhere
+  v.dense = (prob->sic_mode == HCRAN_SIC_DENSE) ? 1 : 0;
+  v.dense_ok = dense_off ? 0 : 1;
   for (int64_t b = first; b < first + count && b < in->B; ++b) {
-    // pass 1: seated-pair SIC family; pass 2 (floor ties only): dense family
-    for (int pass = 0; pass < 2; ++pass) {
-      v.dense = pass;
-      S.load_instance(b);
-      if (mode == 0) S.dinkelbach(b);
-      else S.fixed_e(b);
-      if (!ctl.fg || dense_off) break;
-    }
+    S.load_instance(b);
+    if (mode == 0) S.dinkelbach(b);
+    else S.fixed_e(b);
   }
   free(base);
   free(rbase);

@@ -45,13 +45,13 @@ def lib():
 
 
 def run(cfg, gamma, sigma, mode=0, elastic=None, min_rates=None, e_fixed=None, warm_p=None,
-        dense_off=False, engine=True):
+        dense_off=False, engine=True, exact=False):
     pa = pack.problem_arrays(cfg, sigma)
     ia = pack.instance_arrays(cfg, gamma, elastic, min_rates, e_fixed, warm_p)
     B, M, K, N = ia["gamma"].shape
     T = cfg.tolerances.outer_max
     oa = pack.out_arrays(B, M, K, N, T)
-    prob = pack.problem_struct(cfg, {k: v.ctypes.data for k, v in pa.items()})
+    prob = pack.problem_struct(cfg, {k: v.ctypes.data for k, v in pa.items()}, exact=exact)
     bi = _abi.BatchIn(B=B, gamma=ia["gamma"].ctypes.data, elastic=ia["elastic"].ctypes.data,
                       min_rates=ia["min_rates"].ctypes.data,
                       e_fixed=ia["e_fixed"].ctypes.data if "e_fixed" in ia else None,
