@@ -46,6 +46,8 @@ struct Work {
   // repair scratch
   double *tb, *tX, *tY, *tS, *leaf;  // [MN] x4, leaf [C/64 + 64]
   int32_t* perm;                     // [N]
+  uint8_t *dmask, *tie;              // [N] subcarriers on the dense SIC family / with a floor tie
+  int32_t* dlist;                    // [N] the dense subcarriers, compacted
   // dense SIC pair family (exact mode for floor-tie instances) -- bound when dense
   double *cx, *cxl, *dA, *dB, *nS, *nW, *dg, *ag;  // [C]
   double *pd_zt, *pd_step;                         // [K(K-1)/2][MN] (pair-major)
@@ -88,6 +90,7 @@ struct Work {
     HC_I(mev, M);
     HC_D(tb, MN); HC_D(tX, MN); HC_D(tY, MN); HC_D(tS, MN); HC_D(leaf, C / 64 + 64);
     HC_I(perm, N);
+    HC_B(dmask, N); HC_B(tie, N); HC_I(dlist, N);
     if (dense) {
       const size_t PD = MN * (size_t(K) * (K - 1) / 2);
       HC_D(cx, C); HC_D(cxl, C); HC_D(dA, C); HC_D(dB, C); HC_D(nS, C); HC_D(nW, C);

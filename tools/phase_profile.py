@@ -22,8 +22,10 @@ o = solve_batch(b.cfg, b.gamma, b.sigma)
 lib.hcran_b200_phase_cycles(out, 0)
 names = {0: 'sw:totals+full', 1: 'sw:decode pass', 2: 'sw:utot', 3: 'sw:psi_cross+pairs', 4: 'sw:num/den', 5: 'sw:X1 partials+exchange',
          6: 'sw:bisection', 7: 'sw:closed form', 8: 'sw:X3 exchange', 10: 'round_start', 11: 'round_end', 12: 'run:build_seats',
-         16: 'inner:setup', 17: 'inner:rounds', 18: 'inner:repair', 19: 'inner:feasible'}
-tot = sum(out[i] for i in range(0, 9))
+         16: 'inner:setup', 17: 'inner:rounds', 18: 'inner:repair', 19: 'inner:feasible',
+         20: 'g:totals+full', 21: 'g:decode pass', 22: 'g:utot+psi_cross', 23: 'g:dense terms+hf',
+         24: 'g:num/den', 25: 'g:dense update', 26: 'g:bisection', }
+tot = sum(out[i] for i in list(range(0, 9)) + list(range(20, 27))) or 1
 print('sweeps', int(o['sweeps'].sum().item()), 'instances', nb)
 for i in range(32):
     if out[i]:
