@@ -218,10 +218,21 @@ def load_fp32_peak():
     return 74.4
 
 
+def load_traffic(name, batch):
+    """DRAM bytes (read + write) of the solve kernel for this workload and batch
+    from one `ncu --set full` capture (profiles/ncu_traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f).get(f"{name}:{batch}")
+    return None if d is None else float(d["dram_bytes_per_launch"])
+
+
 def run_b200(args, rank, world, local):
     import torch
     import torch.distributed as dist
-    from paper_1803_07772_b200 import solve_batch
+    from paper_1803_07772_b200 import DeviceProblem, solve_batch
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -232,18 +243,24 @@ def run_b200(args, rank, world, local):
     fixed = name == "c4"
     batch = workload_batch(name, weak_range(rank, B))
     cfg = batch.cfg
-    kw = dict(mode="fixed_e", e_fixed=batch.e_fixed) if fixed else {}
-    el, mr = batch.elastic, batch.min_rates
-    g_dev = torch.from_numpy(batch.gamma).to(dev)
+    # per-instance inputs, pinned on the host (the e2e leg copies them every step)
+    h_in = {"gamma": torch.from_numpy(batch.gamma).pin_memory(),
+            "elastic": torch.from_numpy(np.ascontiguousarray(batch.elastic, np.uint8)).pin_memory(),
+            "min_rates": torch.from_numpy(np.ascontiguousarray(batch.min_rates)).pin_memory()}
+    if fixed:
+        h_in["e_fixed"] = torch.from_numpy(np.ascontiguousarray(batch.e_fixed)).pin_memory()
+    d_in = {k: v.to(dev) for k, v in h_in.items()}
+    problem = DeviceProblem(cfg, batch.sigma, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step(gamma, outputs=None):
-        return solve_batch(cfg, gamma, batch.sigma, el, mr, device=dev, sync=False,
-                           outputs=outputs, **kw)
+    def step(x, outputs=None):
+        kw = dict(mode="fixed_e", e_fixed=x["e_fixed"]) if fixed else {}
+        return solve_batch(cfg, x["gamma"], None, x["elastic"], x["min_rates"], problem=problem,
+                           sync=False, outputs=outputs, **kw)
 
     for _ in range(args.warmup):
-        out = step(g_dev)
+        out = step(d_in)
     torch.cuda.synchronize(dev)
 
     def barrier():
@@ -262,7 +279,7 @@ def run_b200(args, rank, world, local):
     for s in range(args.steps):
         flush.random_(0, 255)  # L2 flush between timed steps (outside the events)
         ev[s][0].record(stream)
-        out = step(g_dev)
+        out = step(d_in)
         ev[s][1].record(stream)
         launches += out["launches"]
         outs.append(out)
@@ -282,25 +299,23 @@ def run_b200(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         want = ["p", "rho", "a", "ee", "sum_rate", "total_power", "status", "outer_iters"]
-        g_host = torch.from_numpy(batch.gamma).pin_memory()
-        host_out = {}
+        o = step(d_in, outputs=want)  # shapes for the pinned result buffers (untimed)
+        host_out = {k: torch.empty(o[k].shape, dtype=o[k].dtype, pin_memory=True) for k in want}
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         d2h = 0
         for s in range(args.steps):
-            o = step(g_host.to(dev, non_blocking=True), outputs=want)
+            o = step(h_in, outputs=want)
             d2h = 0
             for k in want:
                 v = o[k]
-                if k not in host_out:
-                    host_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
                 host_out[k].copy_(v, non_blocking=True)
                 d2h += v.numel() * v.element_size()
         t1.record(stream)
         barrier()
-        h2d = batch.gamma.nbytes + el.size + mr.nbytes
+        h2d = sum(v.numel() * v.element_size() for v in h_in.values())
         te = max_over_ranks(t0.elapsed_time(t1) / 1e3, dev)
         e2e = {"value": world * B * args.steps / te, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
@@ -316,7 +331,8 @@ def run_b200(args, rank, world, local):
                         "Rayleigh x d^-3 gains, seed 1)",
                 "config": workload_desc(name, B),
                 "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
-                             "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                             "unit": "TFLOP/s", "frac": achieved / peak,
+                             "traffic": load_traffic(name, B), "traffic_unit": "DRAM bytes per launch",
                              "peak_source": peak_src,
                              "note": "algorithmic FP64 flop-equivalents counted by the kernel "
                                      "(DESIGN.md work model) / device time of the solve"},

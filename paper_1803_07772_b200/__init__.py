@@ -13,14 +13,14 @@ from .model import (ChannelState, ConfigError, EnergyReport, NetworkConfig,
                     PowerAllocation, Tolerances, UserSpec)
 from .traffic import TrafficSpec, delay_roots, max_delay_from_queue, min_rate_for_delay
 from .scenarios import build_config, gen_channel, tiny_instance, workload_batch
-from .solver import (B200Unavailable, DinkelbachTrace, InfeasibleProblemError, InnerResult,
-                     ScaleSolver, SolveStats, solve, solve_batch)
+from .solver import (B200Unavailable, DeviceProblem, DinkelbachTrace, InfeasibleProblemError,
+                     InnerResult, ScaleSolver, SolveStats, solve, solve_batch)
 
 __all__ = [
     "ChannelState", "ConfigError", "EnergyReport", "NetworkConfig", "PowerAllocation",
     "Tolerances", "UserSpec", "TrafficSpec", "delay_roots", "max_delay_from_queue",
     "min_rate_for_delay", "build_config", "gen_channel", "tiny_instance", "workload_batch",
-    "B200Unavailable", "DinkelbachTrace", "InfeasibleProblemError", "InnerResult",
+    "B200Unavailable", "DeviceProblem", "DinkelbachTrace", "InfeasibleProblemError", "InnerResult",
     "ScaleSolver", "SolveStats", "solve", "solve_batch",
 ]
 

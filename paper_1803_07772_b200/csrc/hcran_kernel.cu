@@ -54,6 +54,10 @@ static __global__ void __launch_bounds__(HCRAN_THREADS, HCRAN_MINB)
 
 static __global__ void __launch_bounds__(RE_THREADS, 1)
     hcran_cluster_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
+#ifdef HCRAN_NO_CLUSTER  // tool builds (profiler): global engine only
+  (void)v; (void)ws; (void)per_cta; (void)counter; (void)mode;
+}
+#else
   extern __shared__ __align__(16) char dsm[];
   __shared__ double red[2 * RE_THREADS / 32];
   __shared__ Ctl ctl;
@@ -100,6 +104,7 @@ static __global__ void __launch_bounds__(RE_THREADS, 1)
     }
   }
 }
+#endif  // HCRAN_NO_CLUSTER
 
 static thread_local int32_t g_last_launches = 0;
 static const size_t HEADER = 256;
@@ -181,6 +186,9 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
   P->dense_all = prob->sic_mode == HCRAN_SIC_DENSE ? 1 : 0;
   if (dn) P->dense_all = atoi(dn);
   if (P->dense_all) cs = 0;
+#ifdef HCRAN_NO_CLUSTER
+  cs = 0;
+#endif
   if (cs > 0) {
     P->engine = 1;
     P->cs = cs;

@@ -59,21 +59,45 @@ def _torch():
 _TORCH_DT = {"f8": "float64", "u1": "uint8", "i4": "int32", "i1": "int8"}
 
 
-class _DeviceProblem:
-    """Batch-constant config arrays resident on the device + the C struct."""
+class DeviceProblem:
+    """Batch-constant config arrays resident on the device + the C struct
+    (hcran_problem_t).  Build once per (config, noise, SIC mode) and pass as
+    `solve_batch(..., problem=)` to keep per-batch host work to the launch."""
 
-    def __init__(self, cfg, sigma, device, exact=False):
+    def __init__(self, cfg, sigma=None, device=None, exact=False):
         torch = _torch()
+        library()
+        if sigma is None:
+            sigma = _flat_sigma(cfg)
         arrs = pack.problem_arrays(cfg, sigma)
-        self.t = {k: torch.from_numpy(np.array(v)).to(device) for k, v in arrs.items()}
+        self.device = torch.device(device or "cuda")
+        self.t = {k: torch.from_numpy(np.array(v)).to(self.device) for k, v in arrs.items()}
         self.struct = pack.problem_struct(cfg, {k: v.data_ptr() for k, v in self.t.items()},
                                           exact=exact)
         self.shape = (cfg.n_rrh, cfg.n_users, cfg.n_subcarriers)
+        self.exact = exact
+
+
+_DeviceProblem = DeviceProblem
+
+
+def _flat_sigma(cfg):
+    M, K, N = cfg.n_rrh, cfg.n_users, cfg.n_subcarriers
+    return np.full((M, K, N), cfg.noise_density * cfg.subcarrier_bandwidth)
+
+
+def _on_device(x, dtype, dev):
+    """numpy / torch (pinned host or device) -> contiguous device tensor, stream-ordered."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x.to(dev, dtype, non_blocking=True).contiguous()
+    np_dt = np.uint8 if dtype == torch.uint8 else np.float64
+    return torch.as_tensor(np.ascontiguousarray(x, np_dt)).to(dev)
 
 
 def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="dinkelbach",
                 e_fixed=None, warm_p=None, stream=None, outputs=None, device=None,
-                workspace=None, sync=True, exact=False):
+                workspace=None, sync=True, exact=False, problem=None):
     """Solve every instance of a batch on the device.
 
     cfg        template NetworkConfig (p_max, p_mask, eta, weights, l_max, tolerances)
@@ -86,32 +110,36 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
                everywhere (HCRAN_SIC_DENSE); "fast": seated family only, floor ties not
                redone (HCRAN_SIC_SEATED_FAST, ~3% of config[1] draws then differ)
     outputs    subset of _abi.OUT_FIELDS names to produce (default: all)
+    problem    a DeviceProblem for (cfg, sigma, exact) built earlier (sigma/exact ignored)
+    Array inputs may be numpy or torch tensors (host tensors should be pinned:
+    they are copied with non_blocking=True on the current stream).
     Returns a dict of CUDA tensors keyed like hcran_batch_out_t (plus "launches").
     """
     torch = _torch()
     lib = library()
-    dev = torch.device(device or "cuda")
-    M, K, N = cfg.n_rrh, cfg.n_users, cfg.n_subcarriers
-    if sigma is None:
-        sigma = np.full((M, K, N), cfg.noise_density * cfg.subcarrier_bandwidth)
-    prob = _DeviceProblem(cfg, sigma, dev, exact=exact)
-    if isinstance(gamma, np.ndarray):
-        g = torch.from_numpy(np.ascontiguousarray(gamma, np.float64)).to(dev)
+    if problem is not None:
+        prob = problem
+        dev = prob.device
     else:
-        g = gamma.to(dev, torch.float64).contiguous()
+        dev = torch.device(device or "cuda")
+        prob = DeviceProblem(cfg, sigma, dev, exact=exact)
+    M, K, N = cfg.n_rrh, cfg.n_users, cfg.n_subcarriers
+    g = _on_device(gamma, torch.float64, dev)
     B = int(g.shape[0])
     if elastic is None:
         elastic = np.broadcast_to(cfg.elastic_mask(), (B, K))
     if min_rates is None:
         min_rates = np.broadcast_to(cfg.min_rates(), (B, K))
-    el = torch.as_tensor(np.ascontiguousarray(elastic, np.uint8)).to(dev)
-    mr = torch.as_tensor(np.ascontiguousarray(min_rates, np.float64)).to(dev)
+    el = _on_device(elastic, torch.uint8, dev)
+    mr = _on_device(min_rates, torch.float64, dev)
     ef = None
     if mode == "fixed_e":
-        ef = torch.as_tensor(np.ascontiguousarray(np.broadcast_to(e_fixed, (B,)), np.float64)).to(dev)
+        if not isinstance(e_fixed, torch.Tensor):
+            e_fixed = np.broadcast_to(e_fixed, (B,))
+        ef = _on_device(e_fixed, torch.float64, dev)
     wp = None
     if warm_p is not None:
-        wp = torch.as_tensor(np.ascontiguousarray(warm_p, np.float64)).to(dev)
+        wp = _on_device(warm_p, torch.float64, dev)
     T = cfg.tolerances.outer_max
     outs = {}
     for name, dt, kind in _abi.OUT_FIELDS:

@@ -5,7 +5,7 @@ sys.path.insert(0, ROOT)
 from paper_1803_07772_b200 import build as B, solver
 lib_path = os.path.join(ROOT, 'tools', 'libhcran_prof.so')
 if not os.path.exists(lib_path):
-    cmd = [B.nvcc()] + B.NVCC_FLAGS + ['-DHCRAN_PROFILE', '-I' + os.path.join(ROOT, 'include'), '-o', lib_path] + B.SOURCES
+    cmd = [B.nvcc()] + B.NVCC_FLAGS + ['-DHCRAN_PROFILE', '-DHCRAN_NO_CLUSTER', '-I' + os.path.join(ROOT, 'include'), '-o', lib_path] + B.SOURCES
     subprocess.run(cmd, check=True, capture_output=True)
 solver.LIB_PATH = lib_path
 lib = solver.library()
@@ -24,7 +24,8 @@ names = {0: 'sw:totals+full', 1: 'sw:decode pass', 2: 'sw:utot', 3: 'sw:psi_cros
          6: 'sw:bisection', 7: 'sw:closed form', 8: 'sw:X3 exchange', 10: 'round_start', 11: 'round_end', 12: 'run:build_seats',
          16: 'inner:setup', 17: 'inner:rounds', 18: 'inner:repair', 19: 'inner:feasible',
          20: 'g:totals+full', 21: 'g:decode pass', 22: 'g:utot+psi_cross', 23: 'g:dense terms+hf',
-         24: 'g:num/den', 25: 'g:dense update', 26: 'g:bisection', }
+         24: 'g:num/den', 25: 'g:dense update', 26: 'g:bisection',
+         27: 'repair:prune+rescale', 28: 'repair:trim', 29: 'repair:boost', 30: 'repair:sic_cleanup', 31: 'repair:final rates'}
 tot = sum(out[i] for i in list(range(0, 9)) + list(range(20, 27))) or 1
 print('sweeps', int(o['sweeps'].sum().item()), 'instances', nb)
 for i in range(32):
