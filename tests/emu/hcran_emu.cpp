@@ -29,6 +29,7 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   v.dense = 0;
   v.flag_int = nullptr;
   v.flag_in = nullptr;
+  v.order = nullptr;
   HostEx ex;
   Ctl ctl;
   memset(&ctl, 0, sizeof(ctl));

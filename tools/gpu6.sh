@@ -1,0 +1,10 @@
+export HCRAN_LIB=tools/variants/lib_order.so
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/variants.txt
+for i in 1 2; do
+python tools/variant_time.py c1 1024 4096 >> gpurun_out/variants.txt 2>&1
+HCRAN_ORDER=0 python tools/variant_time.py c1 1024 4096 >> gpurun_out/variants.txt 2>&1
+done
+python tools/variant_time.py c2 592 2960 >> gpurun_out/variants.txt 2>&1
+HCRAN_ORDER=0 python tools/variant_time.py c2 592 2960 >> gpurun_out/variants.txt 2>&1
+python tools/work_scan.py c2 0 592 > gpurun_out/work_c2.txt 2>&1
