@@ -15,17 +15,23 @@
 using namespace hcran;
 
 #ifndef HCRAN_THREADS
-#define HCRAN_THREADS 256
+#define HCRAN_THREADS 256  // CTA size for instances below HCRAN_BIG_CELLS cells
 #endif
+// Large instances (c2/c3) run 512-thread CTAs (128 registers): twice the
+// memory-level parallelism on their L2-resident state outweighs the spills
+// (+7 % at config[2]); small ones keep 256 threads x 255 registers (-30 % otherwise).
+#define HCRAN_THREADS_BIG 512
+#define HCRAN_BIG_CELLS 16384
 #ifndef HCRAN_MINB
 #define HCRAN_MINB 1
 #endif
 
-static __global__ void __launch_bounds__(HCRAN_THREADS, HCRAN_MINB)
+template <int NT>
+static __global__ void __launch_bounds__(NT, HCRAN_MINB)
     hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
   // pass 1 (v.dense == 0): every instance, seated-pair SIC family, flags floor ties.
   // pass 2 (v.dense == 1): only instances flagged by pass 1, dense pair family.
-  __shared__ double red[2 * HCRAN_THREADS / 32];
+  __shared__ double red[2 * NT / 32];
   __shared__ Ctl ctl;
   __shared__ long long next;
   DevEx ex;
@@ -201,13 +207,19 @@ static int64_t dense_ctas(const hcran_problem_t* p, int64_t B, int64_t grid1) {
   return g;
 }
 
-static int resident_ctas(int device) {
+static bool big_instance(const hcran_problem_t* p) {
+  return (int64_t)p->M * p->K * p->N >= HCRAN_BIG_CELLS;
+}
+
+static int resident_ctas(int device, bool big) {
   int sms = 148, per_sm = 1;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hcran_solve_kernel, HCRAN_THREADS, 0) !=
-          cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
+  const cudaError_t e =
+      big ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, hcran_solve_kernel<HCRAN_THREADS_BIG>, HCRAN_THREADS_BIG, 0)
+          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, hcran_solve_kernel<HCRAN_THREADS>, HCRAN_THREADS, 0);
+  if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   if (per_sm > 8) per_sm = 8;  // state lives in the workspace: bound its footprint
   return sms * per_sm;
 }
@@ -288,7 +300,7 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
     P->engine = 0;
     P->cs = 1;
     P->smem = 0;
-    int64_t g = resident_ctas(device);
+    int64_t g = resident_ctas(device, big_instance(prob));
     if (g > Bp) g = Bp;
     P->slots = g;
     P->grid = g;
@@ -373,8 +385,12 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
         cudaSuccess)
       return HCRAN_E_LAUNCH;
   } else {
-    hcran_solve_kernel<<<(unsigned)P.grid, HCRAN_THREADS, 0, s>>>(v, slots1, P.per, (int*)base,
-                                                                  mode);
+    if (big_instance(prob))
+      hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid, HCRAN_THREADS_BIG, 0, s>>>(
+          v, slots1, P.per, (int*)base, mode);
+    else
+      hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid, HCRAN_THREADS, 0, s>>>(
+          v, slots1, P.per, (int*)base, mode);
   }
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   if (P.grid2 == 0) {  // pass 1 already settled every floor tie (or the fast model ignores them)
@@ -382,8 +398,12 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
     return HCRAN_OK;
   }
   v.dense = 1; v.dense_ok = 0; v.flag_int = nullptr; v.flag_in = flags;
-  hcran_solve_kernel<<<(unsigned)P.grid2, HCRAN_THREADS, 0, s>>>(v, slots2, P.perd, (int*)base + 1,
-                                                                 mode);
+  if (big_instance(prob))
+    hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid2, HCRAN_THREADS_BIG, 0, s>>>(
+        v, slots2, P.perd, (int*)base + 1, mode);
+  else
+    hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid2, HCRAN_THREADS, 0, s>>>(
+        v, slots2, P.perd, (int*)base + 1, mode);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   g_last_launches = launches + 2;
   return HCRAN_OK;

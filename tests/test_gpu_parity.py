@@ -68,6 +68,24 @@ def test_default_mode(golden, devmodel, name):
     assert np.all(o["feasible"][g["feasible"][idx]] == 1)
 
 
+def test_near_tie_draws_mostly_match(golden):
+    """Near-tie draws (the reference itself moves by > 1e-4 under a 1e-12
+    multiplier perturbation) are excused by the parity bar; the host build of
+    the same source matches all 21 of them.  On the device, require most."""
+    tot = hit = 0
+    for name in ("c0", "c1"):
+        g = golden(name)
+        idx = np.nonzero(g["near_tie"])[0]
+        if len(idx) == 0:
+            continue
+        b = workload_batch(name, g["draw"][idx])
+        o = host(solve_batch(b.cfg, b.gamma, b.sigma))
+        hit += sum(bool(_ok(o, g, j, i)) for j, i in enumerate(idx))
+        tot += len(idx)
+    print(f"near-tie draws matching the reference: {hit}/{tot}")
+    assert hit >= 0.8 * tot
+
+
 @pytest.mark.parametrize("name", ["c0", "c1"])
 def test_exact_mode_matches_reference(golden, name):
     """HCRAN_SIC_DENSE: the reference's full SIC family -- every golden
