@@ -137,7 +137,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference instance generator, seed 1)",
-            "config": workload_desc(name, sample), "impl": "reference",
+            "config": workload_desc(name, args.batch or WORKLOADS[name][5]), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{sample} draws of {name} per step, oracle/hcran_oracle.py "
                                        f"(numpy restatement of the reference) in a "
