@@ -29,7 +29,8 @@ struct Work {
   double *full, *utot, *fullm;
   // seats [MN * SMAX]
   double *s_plin, *s_logplin, *s_num, *s_den, *s_psis, *s_cross, *s_inv, *s_rhat, *s_dlog,
-      *s_beta, *s_dsA, *s_dsB, *s_nsS, *s_nsW, *s_dagg, *s_aagg, *s_pround;
+      *s_beta, *s_dsA, *s_dsB, *s_nsS, *s_nsW, *s_dagg, *s_aagg, *s_pround,
+      *s_mask;  // s_mask: the seat's per-cell power cap (mask), set with the seating
   uint8_t* s_user;
   // pairs [MN * NPAIR]
   double *pr_zt, *pr_step, *pr_gconst, *pr_gval, *pr_brk, *pr_slack;
@@ -77,7 +78,7 @@ struct Work {
     HC_D(s_plin, S); HC_D(s_logplin, S); HC_D(s_num, S); HC_D(s_den, S); HC_D(s_psis, S);
     HC_D(s_cross, S); HC_D(s_inv, S); HC_D(s_rhat, S); HC_D(s_dlog, S); HC_D(s_beta, S);
     HC_D(s_dsA, S); HC_D(s_dsB, S); HC_D(s_nsS, S); HC_D(s_nsW, S); HC_D(s_dagg, S);
-    HC_D(s_aagg, S); HC_D(s_pround, S);
+    HC_D(s_aagg, S); HC_D(s_pround, S); HC_D(s_mask, S);
     HC_B(s_user, S);
     HC_D(pr_zt, PP); HC_D(pr_step, PP); HC_D(pr_gconst, PP); HC_D(pr_gval, PP);
     HC_D(pr_brk, PP); HC_D(pr_slack, PP);
