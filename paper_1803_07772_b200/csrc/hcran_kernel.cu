@@ -28,7 +28,7 @@ using namespace hcran;
 
 template <int NT>
 static __global__ void __launch_bounds__(NT, HCRAN_MINB)
-    hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
+    hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode, unsigned hot) {
   // pass 1 (v.dense == 0): every instance, seated-pair SIC family, flags floor ties.
   // pass 2 (v.dense == 1): only instances flagged by pass 1, dense pair family.
   __shared__ double red[2 * NT / 32];
@@ -38,6 +38,8 @@ static __global__ void __launch_bounds__(NT, HCRAN_MINB)
   ex.init(red);
   Work W;
   W.layout(ws + (size_t)blockIdx.x * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0);
+  extern __shared__ __align__(16) char hot_smem[];
+  if (hot) W.bind_hot(hot_smem, hot, (size_t)v.M * v.K * v.N);  // generic pointers: same solver code
   Solver<DevEx> S(ex, v, W, ctl);
   for (;;) {
     if (threadIdx.x == 0) next = (long long)atomicAdd(counter, 1);
@@ -238,11 +240,44 @@ struct Plan {
   int64_t grid2;     // CTAs of pass 2 (dense SIC family)
   size_t perd;
   size_t total;
+  unsigned hot;      // Work::HOT_* arrays bound to dynamic shared memory (global engine)
+  size_t hot_smem;   // their bytes
   int dense_all;     // 1: every instance runs the dense SIC pair family in pass 1
   int dense_ok;      // 1: pass-1 slots carry the dense family (floor ties re-run in place)
 };
 
+// Shared-memory residency of the hottest per-cell arrays (global engine).  The
+// CTA is alone on its SM (255 registers x 256 threads), so its shared memory is
+// otherwise unused; arrays are taken in Work::HOT_* priority order while they
+// fit HCRAN_HOT_KB (default below), the rest stay in the L1/L2-cached slot.
+#ifndef HCRAN_HOT_KB_DEFAULT
+#define HCRAN_HOT_KB_DEFAULT 132  // ord, slot, p, alpha, gam at c1 (+4 %; 172+ starves L1: -5 %..-17 %)
+#endif
+static void choose_hot(const hcran_problem_t* prob, int maxsm, Plan* P) {
+  const char* e = getenv("HCRAN_HOT_KB");
+  size_t budget = (size_t)(e ? atoi(e) : HCRAN_HOT_KB_DEFAULT) * 1024;
+  const size_t cap = (size_t)maxsm - 4096;  // static shared memory of the kernel
+  if (budget > cap) budget = cap;
+  const size_t C = (size_t)prob->M * prob->K * prob->N;
+  P->hot = 0;
+  P->hot_smem = 0;
+  for (int i = 0; i < Work::HOT_N; ++i) {
+    const size_t b = (Work::hot_bytes(i, C) + 15) & ~size_t(15);
+    if (P->hot_smem + b > budget) break;  // keep the priority order: stop at the first misfit
+    P->hot |= 1u << i;
+    P->hot_smem += b;
+  }
+  if (P->hot_smem) {
+    cudaFuncSetAttribute(hcran_solve_kernel<HCRAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)P->hot_smem);
+    cudaFuncSetAttribute(hcran_solve_kernel<HCRAN_THREADS_BIG>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->hot_smem);
+  }
+}
+
 static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P) {
+  P->hot = 0;
+  P->hot_smem = 0;
   const int64_t Bp = B > 0 ? B : 1;
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -300,6 +335,7 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
     P->engine = 0;
     P->cs = 1;
     P->smem = 0;
+    choose_hot(prob, maxsm, P);
     int64_t g = resident_ctas(device, big_instance(prob));
     if (g > Bp) g = Bp;
     P->slots = g;
@@ -386,11 +422,11 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
       return HCRAN_E_LAUNCH;
   } else {
     if (big_instance(prob))
-      hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid, HCRAN_THREADS_BIG, 0, s>>>(
-          v, slots1, P.per, (int*)base, mode);
+      hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid, HCRAN_THREADS_BIG, P.hot_smem, s>>>(
+          v, slots1, P.per, (int*)base, mode, P.hot);
     else
-      hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid, HCRAN_THREADS, 0, s>>>(
-          v, slots1, P.per, (int*)base, mode);
+      hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid, HCRAN_THREADS, P.hot_smem, s>>>(
+          v, slots1, P.per, (int*)base, mode, P.hot);
   }
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   if (P.grid2 == 0) {  // pass 1 already settled every floor tie (or the fast model ignores them)
@@ -399,11 +435,11 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   }
   v.dense = 1; v.dense_ok = 0; v.flag_int = nullptr; v.flag_in = flags;
   if (big_instance(prob))
-    hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid2, HCRAN_THREADS_BIG, 0, s>>>(
-        v, slots2, P.perd, (int*)base + 1, mode);
+    hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid2, HCRAN_THREADS_BIG, P.hot_smem, s>>>(
+        v, slots2, P.perd, (int*)base + 1, mode, P.hot);
   else
-    hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid2, HCRAN_THREADS, 0, s>>>(
-        v, slots2, P.perd, (int*)base + 1, mode);
+    hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid2, HCRAN_THREADS, P.hot_smem, s>>>(
+        v, slots2, P.perd, (int*)base + 1, mode, P.hot);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   g_last_launches = launches + 2;
   return HCRAN_OK;

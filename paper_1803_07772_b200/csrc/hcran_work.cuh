@@ -54,7 +54,34 @@ struct Work {
   double *pd_zt, *pd_step;                         // [K(K-1)/2][MN] (pair-major)
   uint8_t *pq_i, *pq_j;                            // [K(K-1)/2] members of pair q
 
+  double* gam_hot = nullptr;  // shared-memory copy of the instance's gains (bound by the kernel, else null)
+
   HD static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
+
+  // Hot arrays that may live in shared memory instead of the global slot, in
+  // priority order (dependent index loads first).  `hot` is a bit mask over
+  // this list; returns the bytes and rebinds the pointers when base != nullptr.
+  enum { HOT_ORD, HOT_SLOT, HOT_P, HOT_ALPHA, HOT_GAM, HOT_U, HOT_TS, HOT_N };
+  HD static size_t hot_bytes(int i, size_t C) { return (i == HOT_ORD || i == HOT_SLOT) ? C : 8 * C; }
+  HD size_t bind_hot(char* base, unsigned hot, size_t C) {
+    size_t off = 0;
+    for (int i = 0; i < HOT_N; ++i) {
+      if (!(hot & (1u << i))) continue;
+      char* q = base ? base + off : nullptr;
+      off += (hot_bytes(i, C) + 15) & ~size_t(15);
+      if (!base) continue;
+      switch (i) {
+        case HOT_ORD: ord = (uint8_t*)q; break;
+        case HOT_SLOT: slot = (uint8_t*)q; break;
+        case HOT_P: p = (double*)q; break;
+        case HOT_ALPHA: alpha = (double*)q; break;
+        case HOT_GAM: gam_hot = (double*)q; break;
+        case HOT_U: u = (double*)q; break;
+        case HOT_TS: ts = (double*)q; break;
+      }
+    }
+    return off;
+  }
 
   // returns bytes; binds pointers when base != nullptr
   HD size_t layout(char* base, int M, int K, int N, bool dense = false) {
