@@ -165,3 +165,17 @@ def test_sharding_is_order_free():
     half = host(solve_batch(b.cfg, b.gamma[8:], b.sigma))
     assert np.array_equal(full["p"][8:], half["p"])
     assert np.array_equal(full["ee"][8:], half["ee"])
+
+
+@pytest.mark.parametrize("name,kb", [("c1", "0"), ("c1", "212"), ("c2", "100")])
+def test_shared_memory_residency_is_placement_only(golden, monkeypatch, name, kb):
+    """Work::bind_hot moves arrays between global and shared memory; the
+    results must be bit-identical to the default placement."""
+    g = golden(name)
+    idx = np.arange(min(len(g["draw"]), 24))
+    b = workload_batch(name, g["draw"][idx])
+    ref = host(solve_batch(b.cfg, b.gamma, b.sigma))
+    monkeypatch.setenv("HCRAN_HOT_KB", kb)
+    o = host(solve_batch(b.cfg, b.gamma, b.sigma))
+    for k in ("p", "rho", "a", "ee", "total_power", "sweeps", "status", "xi"):
+        assert np.array_equal(o[k], ref[k], equal_nan=True), k
