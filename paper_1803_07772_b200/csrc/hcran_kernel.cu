@@ -251,7 +251,7 @@ struct Plan {
 // otherwise unused; arrays are taken in Work::HOT_* priority order while they
 // fit HCRAN_HOT_KB (default below), the rest stay in the L1/L2-cached slot.
 #ifndef HCRAN_HOT_KB_DEFAULT
-#define HCRAN_HOT_KB_DEFAULT 132  // ord, slot, p, alpha, gam at c1 (+4 %; 172+ starves L1: -5 %..-17 %)
+#define HCRAN_HOT_KB_DEFAULT 92  // ord, slot, p, gains at c1: +6.5 % (adding alpha: +3 %; 172+ KB starves L1: -5..-17 %)
 #endif
 static void choose_hot(const hcran_problem_t* prob, int maxsm, Plan* P) {
   const char* e = getenv("HCRAN_HOT_KB");
@@ -261,7 +261,10 @@ static void choose_hot(const hcran_problem_t* prob, int maxsm, Plan* P) {
   const size_t C = (size_t)prob->M * prob->K * prob->N;
   P->hot = 0;
   P->hot_smem = 0;
+  const char* mk = getenv("HCRAN_HOT_MASK");  // explicit Work::HOT_* bit mask (tuning sweeps)
+  const unsigned want = mk ? (unsigned)strtoul(mk, nullptr, 0) : ~0u;
   for (int i = 0; i < Work::HOT_N; ++i) {
+    if (!(want & (1u << i))) continue;
     const size_t b = (Work::hot_bytes(i, C) + 15) & ~size_t(15);
     if (P->hot_smem + b > budget) break;  // keep the priority order: stop at the first misfit
     P->hot |= 1u << i;

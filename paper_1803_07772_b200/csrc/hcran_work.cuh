@@ -61,7 +61,7 @@ struct Work {
   // Hot arrays that may live in shared memory instead of the global slot, in
   // priority order (dependent index loads first).  `hot` is a bit mask over
   // this list; returns the bytes and rebinds the pointers when base != nullptr.
-  enum { HOT_ORD, HOT_SLOT, HOT_P, HOT_ALPHA, HOT_GAM, HOT_U, HOT_TS, HOT_N };
+  enum { HOT_ORD, HOT_SLOT, HOT_P, HOT_GAM, HOT_ALPHA, HOT_U, HOT_TS, HOT_N };  // profiles/hot_mask_sweep_r01.txt
   HD static size_t hot_bytes(int i, size_t C) { return (i == HOT_ORD || i == HOT_SLOT) ? C : 8 * C; }
   HD size_t bind_hot(char* base, unsigned hot, size_t C) {
     size_t off = 0;
