@@ -51,8 +51,9 @@ extern "C" {
 #define HCRAN_ST_INFEASIBLE 3  /* first inner solve infeasible -> InfeasibleProblemError
                                   (dinkelbach.py:81-86); fixed-e: InnerResult "infeasible" */
 #define HCRAN_ST_OK 0          /* fixed-e: InnerResult "ok" */
-#define HCRAN_ST_UNSUPPORTED 4 /* non-exclusive seating (theta/theta' families live,
-                                  scale.py:566) -- not implemented on the device */
+#define HCRAN_ST_UNSUPPORTED 4 /* device state capacity exceeded: more than 4 seats on one
+                                  (m, n), > 64 tuple rows or > 1024 cross-head seat pairs
+                                  (products-active families, scale.py:566, 861-895) */
 
 /* Tolerances (model.py:59-80); rho1/rho2 already resolved from the mask. */
 typedef struct hcran_tolerances {

@@ -17,6 +17,10 @@ namespace hcran {
 constexpr int SMAX = 4;                       // seats per column (l_max <= 4)
 constexpr int NPAIR = SMAX * (SMAX - 1) / 2;  // seated pairs per column
 constexpr uint8_t NOSLOT = 0xFF;
+// products-active multiplier families (scale.py:761-775, 835-840, 861-895):
+// sparse rows, live only for non-exclusive seatings
+constexpr int TQMAX = 64;    // materialised tuple rows (theta'), per inner solve
+constexpr int THMAX = 1024;  // cross-head seat pairs of one user (theta)
 
 struct Work {
   // dense [C]
@@ -53,10 +57,22 @@ struct Work {
   double *cx, *cxl, *dA, *dB, *nS, *nW, *dg, *ag;  // [C]
   double *pd_zt, *pd_step;                         // [K(K-1)/2][MN] (pair-major)
   uint8_t *pq_i, *pq_j;                            // [K(K-1)/2] members of pair q
+  // products-active families: tuple rows (column, slot mask) and cross-head seat pairs
+  int32_t *tq_col, *th_a, *th_b;                   // [TQMAX], [THMAX] x2 (seat ids)
+  uint8_t* tq_sm;                                  // [TQMAX] member slots (bit mask)
+  double *tq_val, *tq_step, *tq_slack;             // [TQMAX]
+  double *th_val, *th_step, *th_slack;             // [THMAX]
+  double *s_ppair, *s_ptup;                        // [S] per-seat pair / tuple pressure
+  double* pbest;                                   // [C] multistart: best start's end point
 
   double* gam_hot = nullptr;  // shared-memory copy of the instance's gains (bound by the kernel, else null)
 
   HD static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
+  // seats per user the per-user lists hold: a user may sit on several heads
+  // only in small instances (multistart / external warm starts)
+  HD static int useat_cap(int M, int K, int N) {
+    return size_t(M) * K * N <= 4096 ? M * N : N;
+  }
 
   // Hot arrays that may live in shared memory instead of the global slot, in
   // priority order (dependent index loads first).  `hot` is a bit mask over
@@ -113,12 +129,18 @@ struct Work {
     HC_D(zeta, K); HC_D(minr, K); HC_D(score, size_t(M) * K); HC_D(urate, K);
     HC_B(elastic, K); HC_B(hsort, size_t(K) * M); HC_B(best, K);
     HC_I(tried, K); HC_I(needy, K); HC_D(dtmp, K);
-    HC_I(useat, KN); HC_I(ucnt, K);
+    HC_I(useat, size_t(K) * useat_cap(M, K, N)); HC_I(ucnt, K);
     HC_D(xi, M); HC_D(delta, M); HC_D(eps1, M); HC_D(eps2, M); HC_D(mtmp, M);
     HC_I(mev, M);
     HC_D(tb, MN); HC_D(tX, MN); HC_D(tY, MN); HC_D(tS, MN); HC_D(leaf, C / 64 + 64);
     HC_I(perm, N);
     HC_B(dmask, N); HC_B(tie, N); HC_I(dlist, N);
+    HC_I(tq_col, TQMAX); HC_B(tq_sm, TQMAX); HC_D(tq_val, TQMAX); HC_D(tq_step, TQMAX);
+    HC_D(tq_slack, TQMAX);
+    HC_I(th_a, THMAX); HC_I(th_b, THMAX); HC_D(th_val, THMAX); HC_D(th_step, THMAX);
+    HC_D(th_slack, THMAX);
+    HC_D(s_ppair, S); HC_D(s_ptup, S);
+    HC_D(pbest, C <= 4096 ? C : 1);
     if (dense) {
       const size_t PD = MN * (size_t(K) * (K - 1) / 2);
       HC_D(cx, C); HC_D(cxl, C); HC_D(dA, C); HC_D(dB, C); HC_D(nS, C); HC_D(nW, C);

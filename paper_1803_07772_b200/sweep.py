@@ -121,7 +121,10 @@ def run_value(scenario: Scenario, value, solve_batch=None) -> list[DrawResult]:
     res = []
     for d in range(scenario.draws):
         st = int(o["status"][d])
-        if st >= 3:  # InfeasibleProblemError (scenarios.py:248-252) or unsupported seating
+        if st == 4:  # a capacity limit of the device state (hcran_b200.h), not an outcome
+            raise NotImplementedError(f"draw {d}: seating exceeds the device's per-column "
+                                      "seat / tuple capacity (HCRAN_ST_UNSUPPORTED)")
+        if st == 3:  # InfeasibleProblemError (scenarios.py:248-252)
             res.append(DrawResult(value=value, draw=d, feasible=False, wall_s=wall))
             continue
         res.append(DrawResult(value=value, draw=d, feasible=bool(o["feasible"][d]),

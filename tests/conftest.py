@@ -20,7 +20,8 @@ def pytest_configure(config):
 
 def _golden_files(name):
     import glob
-    fs = [f for f in glob.glob(os.path.join(GOLDEN, f"{name}_*_*.npz")) if "_devmodel" not in f]
+    fs = [f for f in glob.glob(os.path.join(GOLDEN, f"{name}_*_*.npz"))
+          if "_devmodel" not in f and "_sel" not in f]
     return sorted(fs, key=lambda f: int(os.path.basename(f).split("_")[1]))
 
 
@@ -43,6 +44,14 @@ def load_golden(name):
     return _concat([dict(np.load(f)) for f in _golden_files(name)])
 
 
+def load_selected(name):
+    """Reference outputs of hand-picked draws (make_golden.py --list): the draws
+    whose device outcome is infeasible, products-active or otherwise rare."""
+    import glob
+    fs = sorted(glob.glob(os.path.join(GOLDEN, f"{name}_*_sel.npz")))
+    return _concat([dict(np.load(f)) for f in fs]) if fs else None
+
+
 def load_devmodel(name):
     """Oracle restatement of the B200 default SIC model for the same draws
     (tests/golden/make_device_model.py); None when not generated."""
@@ -55,6 +64,11 @@ def load_devmodel(name):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+@pytest.fixture(scope="session")
+def selected():
+    return load_selected
 
 
 @pytest.fixture(scope="session")

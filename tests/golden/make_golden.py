@@ -7,6 +7,7 @@ This script is the provenance of every fixture; it is never run on the GPU box
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py c0 --draws 0:128
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py c1 --draws 0:24
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py c4 --draws 0:256
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py c1 --list 598,644,690
 
 Instances are built exactly as `scenarios.run_draw` builds them
 (/root/reference/pkg/src/hcran_noma/scenarios.py:237-242): rng =
@@ -143,6 +144,9 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("config", choices=["c0", "c1", "c2", "c3", "c4"])
     ap.add_argument("--draws", default="0:16")
+    ap.add_argument("--list", default=None,
+                    help="comma-separated draws (e.g. the draws whose device status is "
+                         "infeasible / products-active); written to <config>_<min>_<max+1>_sel.npz")
     ap.add_argument("--workers", type=int, default=max(1, (os.cpu_count() or 2) - 1))
     ap.add_argument("--no-near-tie", action="store_true")
     ap.add_argument("--out", default=None)
@@ -150,8 +154,12 @@ def main(argv=None):
     if args.no_near_tie:
         global NEAR_TIE_REPEATS
         NEAR_TIE_REPEATS = 0
-    lo, hi = (int(x) for x in args.draws.split(":"))
-    draws = list(range(lo, hi))
+    if args.list:
+        draws = sorted(int(x) for x in args.list.split(","))
+        lo, hi = draws[0], draws[-1] + 1
+    else:
+        lo, hi = (int(x) for x in args.draws.split(":"))
+        draws = list(range(lo, hi))
     tasks = [(args.config, d) for d in draws]
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=args.workers) as pool:
@@ -187,8 +195,9 @@ def main(argv=None):
             if v is not None:
                 arr[i, :len(v)] = v
         pack[key] = arr
+    tag = "_sel" if args.list else ""
     out = args.out or os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                                   f"{args.config}_{lo}_{hi}.npz")
+                                   f"{args.config}_{lo}_{hi}{tag}.npz")
     np.savez_compressed(out, **pack)
     print(f"wrote {out}", file=sys.stderr)
 
