@@ -52,9 +52,9 @@ class BatchOut(C.Structure):
     _fields_ = [(name, C.c_void_p) for name, _, _ in OUT_FIELDS]
 
 
-def out_shape(kind: str, B: int, M: int, K: int, N: int, T: int) -> tuple:
+def out_shape(kind: str, B: int, M: int, K: int, N: int, T: int, S: int = 20) -> tuple:
     return {"MKN": (B, M, K, N), "MK": (B, M, K), "": (B,), "M": (B, M), "K": (B, K),
-            "T": (B, T)}[kind]
+            "T": (B, T), "S": (B, S)}[kind]
 
 
 def bind_device_lib(lib: C.CDLL) -> C.CDLL:

@@ -15,8 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhcran_b200.so")
 SOURCES = [os.path.join(CSRC, "hcran_kernel.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("hcran_solver.cuh", "hcran_exec.cuh", "hcran_work.cuh",
-                                           "hcran_rounds.cuh")] + \
+HEADERS = [os.path.join(CSRC, f) for f in ("hcran_solver.cuh", "hcran_exec.cuh", "hcran_work.cuh")] + \
     [os.path.join(ROOT, "include", "hcran_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -25,24 +25,40 @@
 namespace hcran {
 
 #if defined(__CUDACC__)
+// One instance per thread group: `nthr` consecutive threads of the CTA (a
+// warp group of 128, 256 threads, or the whole CTA) solve one instance, so a
+// CTA keeps several independent instances in flight and the warps of one
+// instance waiting at its barriers leave the SM to the others.  Group
+// barriers are named barriers (id 1 + group); the whole-CTA case uses
+// __syncthreads.
 struct DevEx {
-  int tid, nthr, warp, lane, nwarps;
+  int tid, nthr, warp, lane, nwarps, grp;
   static constexpr int WS = 32;
-  double* red;  // shared scratch, >= 2 * nwarps doubles
-  __device__ void init(double* scratch) {
-    tid = threadIdx.x;
-    nthr = blockDim.x;
+  double* red;  // shared scratch of this group, >= 2 * nwarps doubles
+  __device__ void init(double* scratch, int gsize) {
+    grp = threadIdx.x / gsize;
+    tid = threadIdx.x - grp * gsize;
+    nthr = gsize;
     warp = tid >> 5;
     lane = tid & 31;
     nwarps = nthr >> 5;
-    red = scratch;
+    red = scratch + grp * 2 * nwarps;
   }
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ void sync() const {
+    if (nthr == (int)blockDim.x) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthr) : "memory");
+  }
   __device__ __forceinline__ void wsync() const { __syncwarp(); }
-  __device__ __forceinline__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
-  // named barrier over `count` threads (a warp group); id 1..15
-  __device__ __forceinline__ void named_sync(int id, int count) const {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  __device__ __forceinline__ bool any(bool p) const {
+    if (nthr == (int)blockDim.x) return __syncthreads_or(p) != 0;
+    const unsigned v = __any_sync(0xffffffffu, p);
+    int* r = (int*)red;
+    if (lane == 0) r[warp] = v ? 1 : 0;
+    sync();
+    int o = 0;
+    for (int w = 0; w < nwarps; ++w) o |= r[w];
+    sync();
+    return o != 0;
   }
   // warp-level (all lanes receive the result; fixed butterfly order)
   __device__ __forceinline__ double wsum(double v) const {
@@ -61,35 +77,34 @@ struct DevEx {
     return v;
   }
   __device__ __forceinline__ bool wany(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
-  // block-level (all threads receive the result; deterministic order)
+  // group-level (all threads receive the result; deterministic order)
   __device__ double sum(double v) const {
     v = wsum(v);
     if (lane == 0) red[warp] = v;
-    __syncthreads();
+    sync();
     double s = 0.0;
     for (int w = 0; w < nwarps; ++w) s += red[w];
-    __syncthreads();
+    sync();
     return s;
   }
   __device__ double max(double v) const {
     v = wmax(v);
     if (lane == 0) red[warp] = v;
-    __syncthreads();
+    sync();
     double s = red[0];
     for (int w = 1; w < nwarps; ++w) s = fmax(s, red[w]);
-    __syncthreads();
+    sync();
     return s;
   }
 };
 #endif
 
 struct HostEx {
-  int tid = 0, nthr = 1, warp = 0, lane = 0, nwarps = 1;
+  int tid = 0, nthr = 1, warp = 0, lane = 0, nwarps = 1, grp = 0;
   static constexpr int WS = 1;
   void sync() const {}
   void wsync() const {}
   bool any(bool p) const { return p; }
-  void named_sync(int, int) const {}
   double wsum(double v) const { return v; }
   double wmax(double v) const { return v; }
   int wmaxi(int v) const { return v; }

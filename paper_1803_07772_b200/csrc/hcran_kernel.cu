@@ -10,111 +10,64 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
-#include "hcran_rounds.cuh"
+#include "hcran_solver.cuh"
 
 using namespace hcran;
 
-#ifndef HCRAN_THREADS
-#define HCRAN_THREADS 256  // CTA size for instances below HCRAN_BIG_CELLS cells
-#endif
-// Large instances (c2/c3) run 512-thread CTAs (128 registers): twice the
-// memory-level parallelism on their L2-resident state outweighs the spills
-// (+7 % at config[2]); small ones keep 256 threads x 255 registers (-30 % otherwise).
-#define HCRAN_THREADS_BIG 512
-#define HCRAN_BIG_CELLS 16384
-#ifndef HCRAN_MINB
-#define HCRAN_MINB 1
-#endif
+// Launch shapes (threads per CTA NT, threads per instance GT): a CTA of NT
+// threads runs NT / GT independent instances, one per thread group, each
+// pulling instances off the shared queue.  Several instances per SM keep the
+// SM busy while one instance waits at its barriers or on serial phases.
+#define HCRAN_SHAPES(X) X(256, 256) X(512, 512)
 
-template <int NT>
-static __global__ void __launch_bounds__(NT, HCRAN_MINB)
-    hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode, unsigned hot) {
+template <int NT, int GT>
+static __global__ void __launch_bounds__(NT, 1)
+    hcran_solve_kernel(View v, char* ws, size_t per_cta, int* counter, int mode, unsigned hot,
+                       size_t hot_per) {
   // pass 1 (v.dense == 0): every instance, seated-pair SIC family, flags floor ties.
   // pass 2 (v.dense == 1): only instances flagged by pass 1, dense pair family.
+  constexpr int G = NT / GT;
   __shared__ double red[2 * NT / 32];
-  __shared__ Ctl ctl;
-  __shared__ long long next;
+  __shared__ Ctl ctl_s[G];
+  __shared__ long long next_s[G];
   DevEx ex;
-  ex.init(red);
+  ex.init(red, GT);
+  Ctl& ctl = ctl_s[ex.grp];
   Work W;
-  W.layout(ws + (size_t)blockIdx.x * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0);
+  const size_t slot = (size_t)blockIdx.x * G + ex.grp;
+  W.layout(ws + slot * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0, GT / 32);
   extern __shared__ __align__(16) char hot_smem[];
-  if (hot) W.bind_hot(hot_smem, hot, (size_t)v.M * v.K * v.N);  // generic pointers: same solver code
+  if (hot) W.bind_hot(hot_smem + ex.grp * hot_per, hot, v.M, v.K, v.N);  // generic pointers
   Solver<DevEx> S(ex, v, W, ctl);
   for (;;) {
-    if (threadIdx.x == 0) next = (long long)atomicAdd(counter, 1);
-    __syncthreads();
-    const long long q = next;
-    __syncthreads();
+    if (ex.tid == 0) next_s[ex.grp] = (long long)atomicAdd(counter, 1);
+    ex.sync();
+    const long long q = next_s[ex.grp];
+    ex.sync();
     if (q >= v.B) break;
     const long long b = v.order ? (long long)v.order[q] : q;
     if (v.flag_in && !v.flag_in[b]) continue;
     S.load_instance(b);
     if (mode == 0) S.dinkelbach(b);
     else S.fixed_e(b);
-    __syncthreads();
+    ex.sync();
   }
 }
 
-// Cluster kernel: the instance's SCA rounds run on a thread-block cluster whose
-// CTAs hold subcarrier slices in shared memory (hcran_rounds.cuh); the leader
-// CTA (rank 0) runs the outer loop, seating and repair on the global workspace.
-#define RE_THREADS 512
-
-static __global__ void __launch_bounds__(RE_THREADS, 1)
-    hcran_cluster_kernel(View v, char* ws, size_t per_cta, int* counter, int mode) {
-#ifdef HCRAN_NO_CLUSTER  // tool builds (profiler): global engine only
-  (void)v; (void)ws; (void)per_cta; (void)counter; (void)mode;
-}
-#else
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ double red[2 * RE_THREADS / 32];
-  __shared__ Ctl ctl;
-  __shared__ ReCmd cmd;
-  __shared__ long long next;
-  DevEx ex;
-  ex.init(red);
-  ClusterDev cx;
-  cx.init();
-  ReMem R;
-  R.layout(dsm, v.M, v.K, v.N / cx.csize, v.L, v.N, RE_THREADS / 32);
-  Rounds<DevEx, ClusterDev> RE(ex, cx, v, R);
-  const int cid = blockIdx.x / cx.csize;
-  Work W;
-  W.layout(ws + (size_t)cid * per_cta, v.M, v.K, v.N, false);
-  if (cx.crank == 0) {
-    Solver<DevEx, Rounds<DevEx, ClusterDev>> S(ex, v, W, ctl);
-    S.re = &RE;
-    S.re_cmd = &cmd;
-    for (;;) {
-      if (threadIdx.x == 0) next = (long long)atomicAdd(counter, 1);
-      __syncthreads();
-      const long long q = next;
-      __syncthreads();
-      if (q >= v.B) break;
-      const long long b = v.order ? (long long)v.order[q] : q;
-      S.load_instance(b);
-      if (mode == 0) S.dinkelbach(b);
-      else S.fixed_e(b);
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) cmd.op = 0;
-    __threadfence();
-    cx.csync();  // publish EXIT
-    cx.csync();  // keep this CTA's shared memory alive until every follower has read it
-  } else {
-    for (;;) {
-      cx.csync();
-      const ReCmd c = *cx.remote(&cmd, 0);
-      if (c.op == 0) {
-        cx.csync();
-        break;
-      }
-      RE.run(c, W.p);
-    }
+struct Shape {
+  int nt, gt;
+};
+// default shape per instance size (cells); HCRAN_SHAPE=NT:GT overrides
+static Shape shape_of(const hcran_problem_t* p) {
+  const char* e = getenv("HCRAN_SHAPE");
+  if (e) {
+    Shape s{0, 0};
+    if (sscanf(e, "%d:%d", &s.nt, &s.gt) == 2) return s;
   }
+  const int64_t cells = (int64_t)p->M * p->K * p->N;
+  if (cells >= 16384) return Shape{512, 512};
+  return Shape{256, 256};
 }
-#endif  // HCRAN_NO_CLUSTER
 
 // ---------------------------------------------------------------- queue order
 // Per-instance work varies ~10x and the persistent queue
@@ -191,9 +144,10 @@ static int check_problem(const hcran_problem_t* p) {
   return HCRAN_OK;
 }
 
+// workspace bytes of one instance slot
 static size_t per_cta_bytes(const hcran_problem_t* p, bool dense = false) {
   Work w;
-  return w.layout(nullptr, p->M, p->K, p->N, dense);
+  return w.layout(nullptr, p->M, p->K, p->N, dense, shape_of(p).gt / 32);
 }
 
 static size_t flags_bytes(int64_t B) { return ((size_t)B + 255) & ~(size_t)255; }
@@ -201,7 +155,7 @@ static size_t order_bytes(int64_t B) { return 2 * (((size_t)B * 4 + 255) & ~(siz
 
 // CTAs for the dense re-solve pass: a few per SM at most, bounded to ~4 GiB of state
 static int64_t dense_ctas(const hcran_problem_t* p, int64_t B, int64_t grid1) {
-  size_t per = per_cta_bytes(p, true);
+  size_t per = per_cta_bytes(p, true) * (shape_of(p).nt / shape_of(p).gt);
   int64_t g = (int64_t)(((size_t)4 << 30) / per);
   if (g > grid1) g = grid1;
   if (g > B) g = B;
@@ -209,149 +163,99 @@ static int64_t dense_ctas(const hcran_problem_t* p, int64_t B, int64_t grid1) {
   return g;
 }
 
-static bool big_instance(const hcran_problem_t* p) {
-  return (int64_t)p->M * p->K * p->N >= HCRAN_BIG_CELLS;
+typedef void (*KernelFn)(View, char*, size_t, int*, int, unsigned, size_t);
+static KernelFn kernel_of(Shape s) {
+#define HC_PICK(a, b) if (s.nt == a && s.gt == b) return hcran_solve_kernel<a, b>;
+  HCRAN_SHAPES(HC_PICK)
+#undef HC_PICK
+  return nullptr;
 }
 
-static int resident_ctas(int device, bool big) {
+// resident CTAs (one per SM: the kernels are register-bound at NT threads)
+static int resident_ctas(int device, Shape sh, size_t smem) {
   int sms = 148, per_sm = 1;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) sms = 148;
-  const cudaError_t e =
-      big ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, hcran_solve_kernel<HCRAN_THREADS_BIG>, HCRAN_THREADS_BIG, 0)
-          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, hcran_solve_kernel<HCRAN_THREADS>, HCRAN_THREADS, 0);
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_of(sh), sh.nt, smem);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   if (per_sm > 8) per_sm = 8;  // state lives in the workspace: bound its footprint
   return sms * per_sm;
 }
 
-static size_t re_smem(const hcran_problem_t* p, int cs) {
-  ReMem r;
-  return r.layout(nullptr, p->M, p->K, p->N / cs, p->l_max, p->N, RE_THREADS / 32);
-}
-
 struct Plan {
-  int engine;        // 1: cluster rounds engine, 0: global-workspace engine
-  int cs;            // cluster size
   int64_t grid;      // CTAs of pass 1
-  int64_t slots;     // pass-1 workspace slots (clusters or CTAs)
-  size_t per, smem;  // bytes per slot / dynamic smem per CTA
+  int64_t slots;     // pass-1 workspace slots (one per CTA)
+  size_t per;        // bytes per slot
   int64_t grid2;     // CTAs of pass 2 (dense SIC family)
   size_t perd;
   size_t total;
-  unsigned hot;      // Work::HOT_* arrays bound to dynamic shared memory (global engine)
-  size_t hot_smem;   // their bytes
+  unsigned hot;      // Work::HOT_* arrays bound to dynamic shared memory
+  size_t hot_smem;   // their bytes per CTA
+  size_t hot_per;    // ... per instance (thread group)
+  Shape sh;          // launch shape
+  int groups;        // instances per CTA
   int dense_all;     // 1: every instance runs the dense SIC pair family in pass 1
   int dense_ok;      // 1: pass-1 slots carry the dense family (floor ties re-run in place)
 };
 
-// Shared-memory residency of the hottest per-cell arrays (global engine).  The
-// CTA is alone on its SM (255 registers x 256 threads), so its shared memory is
-// otherwise unused; arrays are taken in Work::HOT_* priority order while they
-// fit HCRAN_HOT_KB (default below), the rest stay in the L1/L2-cached slot.
+// Shared-memory residency: the per-sweep streams of the analysis (decode
+// ranks, gains, bound slopes, ...) are bound to dynamic shared memory in
+// Work::HOT_* priority order while they fit the instance's share of
+// HCRAN_HOT_KB (per CTA); an array that does not fit is skipped, the rest stay
+// in the L1/L2-cached slot.
 #ifndef HCRAN_HOT_KB_DEFAULT
-#define HCRAN_HOT_KB_DEFAULT 92  // ord, slot, p, gains at c1: +6.5 % (adding alpha: +3 %; 172+ KB starves L1: -5..-17 %)
+#define HCRAN_HOT_KB_DEFAULT 16
 #endif
 static void choose_hot(const hcran_problem_t* prob, int maxsm, Plan* P) {
   const char* e = getenv("HCRAN_HOT_KB");
   size_t budget = (size_t)(e ? atoi(e) : HCRAN_HOT_KB_DEFAULT) * 1024;
-  const size_t cap = (size_t)maxsm - 4096;  // static shared memory of the kernel
+  const size_t cap = (size_t)maxsm - 8192;  // static shared memory of the kernel
   if (budget > cap) budget = cap;
-  const size_t C = (size_t)prob->M * prob->K * prob->N;
+  budget /= P->groups;
   P->hot = 0;
-  P->hot_smem = 0;
+  P->hot_per = 0;
   const char* mk = getenv("HCRAN_HOT_MASK");  // explicit Work::HOT_* bit mask (tuning sweeps)
   const unsigned want = mk ? (unsigned)strtoul(mk, nullptr, 0) : ~0u;
   for (int i = 0; i < Work::HOT_N; ++i) {
     if (!(want & (1u << i))) continue;
-    const size_t b = (Work::hot_bytes(i, C) + 15) & ~size_t(15);
-    if (P->hot_smem + b > budget) break;  // keep the priority order: stop at the first misfit
+    const size_t b = (Work::hot_bytes(i, prob->M, prob->K, prob->N) + 15) & ~size_t(15);
+    if (P->hot_per + b > budget) continue;
     P->hot |= 1u << i;
-    P->hot_smem += b;
+    P->hot_per += b;
   }
-  if (P->hot_smem) {
-    cudaFuncSetAttribute(hcran_solve_kernel<HCRAN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)P->hot_smem);
-    cudaFuncSetAttribute(hcran_solve_kernel<HCRAN_THREADS_BIG>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->hot_smem);
-  }
+  P->hot_smem = P->hot_per * P->groups;
+  if (P->hot_smem) cudaFuncSetAttribute(kernel_of(P->sh), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)P->hot_smem);
 }
 
 static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P) {
   P->hot = 0;
   P->hot_smem = 0;
+  P->sh = shape_of(prob);
+  if (!kernel_of(P->sh)) return HCRAN_E_ARG;
+  P->groups = P->sh.nt / P->sh.gt;
   const int64_t Bp = B > 0 ? B : 1;
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (maxsm <= 0) maxsm = 232448;
-  const size_t budget = (size_t)maxsm - 2048;  // static shared memory of the kernel
-  int cs = 0;
-  const char* force = getenv("HCRAN_CLUSTER");
-  const int want = force ? atoi(force) : -1;  // default: global-workspace engine (faster)
-  for (int c = 1; c <= 16; c <<= 1) {
-    if (prob->N % c) continue;
-    if (want > 0 && c != want) continue;
-    if (want < 0) break;  // HCRAN_CLUSTER=-1: force the global engine
-    if (re_smem(prob, c) <= budget) { cs = c; break; }
-  }
   P->perd = per_cta_bytes(prob, true);
   P->dense_ok = 0;
   const char* dn = getenv("HCRAN_DENSE");
   P->dense_all = prob->sic_mode == HCRAN_SIC_DENSE ? 1 : 0;
   if (dn) P->dense_all = atoi(dn);
-  if (P->dense_all) cs = 0;
-#ifdef HCRAN_NO_CLUSTER
-  cs = 0;
-#endif
-  if (cs > 0) {
-    P->engine = 1;
-    P->cs = cs;
-    P->smem = re_smem(prob, cs);
-    P->per = per_cta_bytes(prob);
-    cudaFuncSetAttribute(hcran_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)P->smem);
-    if (cs > 8) cudaFuncSetAttribute(hcran_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs * 64);
-    cfg.blockDim = dim3(RE_THREADS);
-    cfg.dynamicSmemBytes = P->smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, hcran_cluster_kernel, &cfg) != cudaSuccess || ncl < 1) {
-      cudaGetLastError();
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      ncl = sms / cs;
-    }
-    int64_t nc = ncl;
-    if (nc > Bp) nc = Bp;
-    P->slots = nc;
-    P->grid = nc * cs;
-  } else {
-    P->engine = 0;
-    P->cs = 1;
-    P->smem = 0;
-    choose_hot(prob, maxsm, P);
-    int64_t g = resident_ctas(device, big_instance(prob));
-    if (g > Bp) g = Bp;
-    P->slots = g;
-    P->grid = g;
-    // floor ties are re-run in place when every slot can carry the dense family
-    P->dense_ok = (!P->dense_all && prob->sic_mode != HCRAN_SIC_SEATED_FAST &&
-                   (size_t)g * P->perd <= ((size_t)24 << 30)) ? 1 : 0;
-    P->per = per_cta_bytes(prob, P->dense_all != 0 || P->dense_ok != 0);
-  }
+  choose_hot(prob, maxsm, P);
+  int64_t g = resident_ctas(device, P->sh, P->hot_smem);
+  const int64_t gneed = (Bp + P->groups - 1) / P->groups;
+  if (g > gneed) g = gneed;
+  P->grid = g;
+  P->slots = g * P->groups;
+  // floor ties are re-run in place when every slot can carry the dense family
+  P->dense_ok = (!P->dense_all && prob->sic_mode != HCRAN_SIC_SEATED_FAST &&
+                 (size_t)P->slots * P->perd <= ((size_t)24 << 30)) ? 1 : 0;
+  P->per = per_cta_bytes(prob, P->dense_all != 0 || P->dense_ok != 0);
   P->grid2 = (P->dense_all || P->dense_ok || prob->sic_mode == HCRAN_SIC_SEATED_FAST)
                  ? 0 : dense_ctas(prob, Bp, P->grid);
   P->total = HEADER + flags_bytes(Bp) + order_bytes(Bp) + (size_t)P->slots * P->per +
-             (size_t)P->grid2 * P->perd;
+             (size_t)P->grid2 * P->groups * P->perd;
   return HCRAN_OK;
 }
 
@@ -378,7 +282,8 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   int device = 0;
   cudaGetDevice(&device);
   Plan P;
-  make_plan(prob, in->B, device, &P);
+  rc = make_plan(prob, in->B, device, &P);
+  if (rc) return rc;
   if (ws_bytes < P.total) return HCRAN_E_WORKSPACE;
   View v;
   v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
@@ -407,42 +312,16 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
     v.order = order;
     launches = 3;
   }
-  if (P.engine == 1) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)P.grid);
-    cfg.blockDim = dim3(RE_THREADS);
-    cfg.dynamicSmemBytes = P.smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = P.cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, hcran_cluster_kernel, v, slots1, P.per, (int*)base, mode) !=
-        cudaSuccess)
-      return HCRAN_E_LAUNCH;
-  } else {
-    if (big_instance(prob))
-      hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid, HCRAN_THREADS_BIG, P.hot_smem, s>>>(
-          v, slots1, P.per, (int*)base, mode, P.hot);
-    else
-      hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid, HCRAN_THREADS, P.hot_smem, s>>>(
-          v, slots1, P.per, (int*)base, mode, P.hot);
-  }
+  const KernelFn kfn = kernel_of(P.sh);
+  kfn<<<(unsigned)P.grid, P.sh.nt, P.hot_smem, s>>>(v, slots1, P.per, (int*)base, mode, P.hot, P.hot_per);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   if (P.grid2 == 0) {  // pass 1 already settled every floor tie (or the fast model ignores them)
     g_last_launches = launches + 1;
     return HCRAN_OK;
   }
   v.dense = 1; v.dense_ok = 0; v.flag_int = nullptr; v.flag_in = flags;
-  if (big_instance(prob))
-    hcran_solve_kernel<HCRAN_THREADS_BIG><<<(unsigned)P.grid2, HCRAN_THREADS_BIG, P.hot_smem, s>>>(
-        v, slots2, P.perd, (int*)base + 1, mode, P.hot);
-  else
-    hcran_solve_kernel<HCRAN_THREADS><<<(unsigned)P.grid2, HCRAN_THREADS, P.hot_smem, s>>>(
-        v, slots2, P.perd, (int*)base + 1, mode, P.hot);
+  kfn<<<(unsigned)P.grid2, P.sh.nt, P.hot_smem, s>>>(v, slots2, P.perd, (int*)base + 1, mode, P.hot,
+                                                     P.hot_per);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   g_last_launches = launches + 2;
   return HCRAN_OK;
@@ -454,9 +333,9 @@ extern "C" int hcran_b200_engine(const hcran_problem_t* prob, int64_t B, int dev
   if (rc) return rc;
   Plan P;
   make_plan(prob, B, device, &P);
-  if (engine) *engine = P.engine;
-  if (cluster) *cluster = P.cs;
-  if (smem) *smem = P.smem;
+  if (engine) *engine = 0;   // one CTA per instance (the cluster engine of round 1 is gone)
+  if (cluster) *cluster = 1;
+  if (smem) *smem = P.hot_smem;
   return HCRAN_OK;
 }
 

@@ -23,9 +23,13 @@ constexpr int TQMAX = 64;    // materialised tuple rows (theta'), per inner solv
 constexpr int THMAX = 1024;  // cross-head seat pairs of one user (theta)
 
 struct Work {
-  // dense [C]
-  double *p, *pacc, *alpha, *u, *ts;
-  uint8_t *ord, *rnk, *slot, *flag;
+  // dense [C], reference order [m][k][n]
+  double *p, *pacc, *alpha, *u;  // alpha: bound slope per round; u: scratch copy of p
+  uint8_t *ord, *rnk, *slot, *flag;  // rnk: decode rank (# stronger users on (m, n))
+  // column tables of the analysis: seat ranks ascending [MN][SMAX], prefix
+  // sums of the seat powers in that order [MN][SMAX + 1]
+  uint8_t* cs_r;
+  double* cs_q;
   // columns [MN]
   double *tot, *pcross, *fterm, *dcross, *bterm, *mtot, *colmax;
   uint8_t *ncnt, *npr;
@@ -34,7 +38,8 @@ struct Work {
   // seats [MN * SMAX]
   double *s_plin, *s_logplin, *s_num, *s_den, *s_psis, *s_cross, *s_inv, *s_rhat, *s_dlog,
       *s_beta, *s_dsA, *s_dsB, *s_nsS, *s_nsW, *s_dagg, *s_aagg, *s_pround,
-      *s_mask;  // s_mask: the seat's per-cell power cap (mask), set with the seating
+      *s_mask,   // s_mask: the seat's per-cell power cap (mask), set with the seating
+      *s_alpha;  // the seat's bound slope (per round)
   uint8_t* s_user;
   // pairs [MN * NPAIR]
   double *pr_zt, *pr_step, *pr_gconst, *pr_gval, *pr_brk, *pr_slack;
@@ -52,6 +57,9 @@ struct Work {
   double *tb, *tX, *tY, *tS, *leaf;  // [MN] x4, leaf [C/64 + 64]
   int32_t* perm;                     // [N]
   uint8_t *dmask, *tie;              // [N] subcarriers on the dense SIC family / with a floor tie
+  // repair: the nonzero cells of each column (<= l_max after the top-l cut),
+  // users in index order (nzu) and in decode order (nzr); nzc 255 = not sparse
+  uint8_t *nzu, *nzr, *nzc;
   int32_t* dlist;                    // [N] the dense subcarriers, compacted
   // dense SIC pair family (exact mode for floor-tie instances) -- bound when dense
   double *cx, *cxl, *dA, *dB, *nS, *nW, *dg, *ag;  // [C]
@@ -65,6 +73,10 @@ struct Work {
   double *s_ppair, *s_ptup;                        // [S] per-seat pair / tuple pressure
   double* pbest;                                   // [C] multistart: best start's end point
 
+  double* wleaf;    // [nw][wlstride]: leaf sums of the warp-parallel pairwise sums
+  int32_t* wleafi;  // [nw][wlstride]: their offsets (PwCache)
+  int wlstride;
+  int nwarps = 1;
   double* gam_hot = nullptr;  // shared-memory copy of the instance's gains (bound by the kernel, else null)
 
   HD static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
@@ -74,34 +86,52 @@ struct Work {
     return size_t(M) * K * N <= 4096 ? M * N : N;
   }
 
-  // Hot arrays that may live in shared memory instead of the global slot, in
-  // priority order (dependent index loads first).  `hot` is a bit mask over
-  // this list; returns the bytes and rebinds the pointers when base != nullptr.
-  enum { HOT_ORD, HOT_SLOT, HOT_P, HOT_GAM, HOT_ALPHA, HOT_U, HOT_TS, HOT_N };  // profiles/hot_mask_sweep_r01.txt
-  HD static size_t hot_bytes(int i, size_t C) { return (i == HOT_ORD || i == HOT_SLOT) ? C : 8 * C; }
-  HD size_t bind_hot(char* base, unsigned hot, size_t C) {
+  // Arrays that may live in shared memory instead of the global slot, in
+  // priority order: the analysis' column / row tables (read for every cell in
+  // every sweep), then the per-cell streams.  `hot` is a bit mask over this
+  // list; returns the bytes and rebinds the pointers when base != nullptr.
+  enum { HOT_CSR, HOT_CSQ, HOT_TOT, HOT_FULL, HOT_UTOT, HOT_RNK, HOT_GAM, HOT_ALPHA, HOT_U,
+         HOT_SLOT, HOT_P, HOT_N };
+  HD static size_t hot_bytes(int i, size_t M, size_t K, size_t N) {
+    const size_t C = M * K * N;
+    switch (i) {
+      case HOT_CSR: return M * N * SMAX;
+      case HOT_CSQ: return 8 * M * N * (SMAX + 1);
+      case HOT_TOT: return 8 * M * N;
+      case HOT_FULL: case HOT_UTOT: return 8 * K * N;
+      case HOT_RNK: case HOT_SLOT: return C;
+      default: return 8 * C;
+    }
+  }
+  HD size_t bind_hot(char* base, unsigned hot, int M, int K, int N) {
     size_t off = 0;
     for (int i = 0; i < HOT_N; ++i) {
       if (!(hot & (1u << i))) continue;
       char* q = base ? base + off : nullptr;
-      off += (hot_bytes(i, C) + 15) & ~size_t(15);
+      off += (hot_bytes(i, M, K, N) + 15) & ~size_t(15);
       if (!base) continue;
       switch (i) {
-        case HOT_ORD: ord = (uint8_t*)q; break;
+        case HOT_CSR: cs_r = (uint8_t*)q; break;
+        case HOT_CSQ: cs_q = (double*)q; break;
+        case HOT_TOT: tot = (double*)q; break;
+        case HOT_FULL: full = (double*)q; break;
+        case HOT_UTOT: utot = (double*)q; break;
+        case HOT_RNK: rnk = (uint8_t*)q; break;
+        case HOT_GAM: gam_hot = (double*)q; break;
+        case HOT_ALPHA: alpha = (double*)q; break;
+        case HOT_U: u = (double*)q; break;
         case HOT_SLOT: slot = (uint8_t*)q; break;
         case HOT_P: p = (double*)q; break;
-        case HOT_ALPHA: alpha = (double*)q; break;
-        case HOT_GAM: gam_hot = (double*)q; break;
-        case HOT_U: u = (double*)q; break;
-        case HOT_TS: ts = (double*)q; break;
       }
     }
     return off;
   }
 
   // returns bytes; binds pointers when base != nullptr
-  HD size_t layout(char* base, int M, int K, int N, bool dense = false) {
+  HD size_t layout(char* base, int M, int K, int N, bool dense = false, int nw = 16) {
     const size_t C = size_t(M) * K * N, MN = size_t(M) * N, KN = size_t(K) * N;
+    nwarps = nw;
+    wlstride = K * N / 64 + 8;
     const size_t S = MN * SMAX, PP = MN * NPAIR;
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
@@ -112,8 +142,10 @@ struct Work {
 #define HC_D(name, n) name = (double*)take(sizeof(double) * (n))
 #define HC_B(name, n) name = (uint8_t*)take(n)
 #define HC_I(name, n) name = (int32_t*)take(sizeof(int32_t) * (n))
-    HC_D(p, C); HC_D(pacc, C); HC_D(alpha, C); HC_D(u, C); HC_D(ts, C);
+    HC_D(p, C); HC_D(pacc, C); HC_D(alpha, C); HC_D(u, C);
     HC_B(ord, C); HC_B(rnk, C); HC_B(slot, C); HC_B(flag, C);
+    HC_B(cs_r, MN * SMAX); HC_D(cs_q, MN * (SMAX + 1));
+    HC_D(wleaf, size_t(nw) * wlstride); HC_I(wleafi, size_t(nw) * wlstride);
     HC_D(tot, MN); HC_D(pcross, MN); HC_D(fterm, MN); HC_D(dcross, MN); HC_D(bterm, MN);
     HC_D(mtot, MN); HC_D(colmax, MN);
     HC_B(ncnt, MN); HC_B(npr, MN);
@@ -121,7 +153,7 @@ struct Work {
     HC_D(s_plin, S); HC_D(s_logplin, S); HC_D(s_num, S); HC_D(s_den, S); HC_D(s_psis, S);
     HC_D(s_cross, S); HC_D(s_inv, S); HC_D(s_rhat, S); HC_D(s_dlog, S); HC_D(s_beta, S);
     HC_D(s_dsA, S); HC_D(s_dsB, S); HC_D(s_nsS, S); HC_D(s_nsW, S); HC_D(s_dagg, S);
-    HC_D(s_aagg, S); HC_D(s_pround, S); HC_D(s_mask, S);
+    HC_D(s_aagg, S); HC_D(s_pround, S); HC_D(s_mask, S); HC_D(s_alpha, S);
     HC_B(s_user, S);
     HC_D(pr_zt, PP); HC_D(pr_step, PP); HC_D(pr_gconst, PP); HC_D(pr_gval, PP);
     HC_D(pr_brk, PP); HC_D(pr_slack, PP);
@@ -135,6 +167,7 @@ struct Work {
     HC_D(tb, MN); HC_D(tX, MN); HC_D(tY, MN); HC_D(tS, MN); HC_D(leaf, C / 64 + 64);
     HC_I(perm, N);
     HC_B(dmask, N); HC_B(tie, N); HC_I(dlist, N);
+    HC_B(nzu, MN * SMAX); HC_B(nzr, MN * SMAX); HC_B(nzc, MN);
     HC_I(tq_col, TQMAX); HC_B(tq_sm, TQMAX); HC_D(tq_val, TQMAX); HC_D(tq_step, TQMAX);
     HC_D(tq_slack, TQMAX);
     HC_I(th_a, THMAX); HC_I(th_b, THMAX); HC_D(th_val, THMAX); HC_D(th_step, THMAX);

@@ -117,12 +117,23 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
     """
     torch = _torch()
     lib = library()
-    if problem is not None:
-        prob = problem
-        dev = prob.device
-    else:
-        dev = torch.device(device or "cuda")
-        prob = DeviceProblem(cfg, sigma, dev, exact=exact)
+    dev = problem.device if problem is not None else torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    # every allocation, copy and the launch are ordered on `s`, with `dev` current
+    # (the library launches on the calling thread's current device)
+    with torch.cuda.device(dev), torch.cuda.stream(s):
+        outs = _solve_batch_on(torch, lib, dev, s, cfg, gamma, sigma, elastic, min_rates, mode,
+                               e_fixed, warm_p, outputs, workspace, exact, problem)
+    if sync:
+        s.synchronize()
+    return outs
+
+
+def _solve_batch_on(torch, lib, dev, s, cfg, gamma, sigma, elastic, min_rates, mode, e_fixed,
+                    warm_p, outputs, workspace, exact, problem):
+    prob = problem if problem is not None else DeviceProblem(cfg, sigma, dev, exact=exact)
     M, K, N = cfg.n_rrh, cfg.n_users, cfg.n_subcarriers
     g = _on_device(gamma, torch.float64, dev)
     B = int(g.shape[0])
@@ -145,19 +156,18 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
     for name, dt, kind in _abi.OUT_FIELDS:
         if outputs is not None and name not in outputs:
             continue
-        outs[name] = torch.empty(_abi.out_shape(kind, B, M, K, N, T),
+        outs[name] = torch.empty(_abi.out_shape(kind, B, M, K, N, T, cfg.tolerances.s_max),
                                  dtype=getattr(torch, _TORCH_DT[dt]), device=dev)
     bi = _abi.BatchIn(B=B, gamma=g.data_ptr(), elastic=el.data_ptr(), min_rates=mr.data_ptr(),
                       e_fixed=ef.data_ptr() if ef is not None else None,
                       warm_p=wp.data_ptr() if wp is not None else None)
     bo = _abi.BatchOut(**{k: v.data_ptr() for k, v in outs.items()})
     grid, wsb = C.c_int32(), C.c_size_t()
-    rc = lib.hcran_b200_plan(C.byref(prob.struct), B, dev.index or 0, C.byref(grid), C.byref(wsb))
+    rc = lib.hcran_b200_plan(C.byref(prob.struct), B, dev.index, C.byref(grid), C.byref(wsb))
     if rc:
         raise ValueError(f"hcran_b200_plan: {_abi.ERRORS.get(rc, rc)}")
     if workspace is None or workspace.numel() < wsb.value:
         workspace = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
     fn = lib.hcran_b200_solve_batch if mode == "dinkelbach" else lib.hcran_b200_solve_fixed_e_batch
     rc = fn(C.byref(prob.struct), C.byref(bi), C.byref(bo), workspace.data_ptr(), wsb.value,
             s.cuda_stream)
@@ -165,8 +175,6 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
         raise RuntimeError(f"hcran_b200 solve failed: {_abi.ERRORS.get(rc, rc)}")
     outs["launches"] = int(lib.hcran_b200_last_launches())
     outs["_keepalive"] = (prob, g, el, mr, ef, wp, workspace)
-    if sync:
-        s.synchronize()
     return outs
 
 

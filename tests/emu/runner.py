@@ -17,8 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 SRC = os.path.join(HERE, "hcran_emu.cpp")
 LIB = os.path.join(HERE, "libhcran_emu.so")
 DEPS = [SRC] + [os.path.join(ROOT, "paper_1803_07772_b200", "csrc", f)
-                for f in ("hcran_solver.cuh", "hcran_exec.cuh", "hcran_work.cuh",
-                          "hcran_rounds.cuh")] + \
+                for f in ("hcran_solver.cuh", "hcran_exec.cuh", "hcran_work.cuh")] + \
        [os.path.join(ROOT, "include", "hcran_b200.h")]
 
 _lib = None
@@ -39,13 +38,13 @@ def lib():
         _lib = C.CDLL(build())
         _lib.hcran_emu_solve.argtypes = [C.POINTER(_abi.Problem), C.POINTER(_abi.BatchIn),
                                          C.POINTER(_abi.BatchOut), C.c_int, C.c_int64,
-                                         C.c_int64, C.c_int, C.c_int]
+                                         C.c_int64, C.c_int]
         _lib.hcran_emu_solve.restype = C.c_int
     return _lib
 
 
 def run(cfg, gamma, sigma, mode=0, elastic=None, min_rates=None, e_fixed=None, warm_p=None,
-        dense_off=False, engine=True, exact=False):
+        dense_off=False, exact=False):
     pa = pack.problem_arrays(cfg, sigma)
     ia = pack.instance_arrays(cfg, gamma, elastic, min_rates, e_fixed, warm_p)
     B, M, K, N = ia["gamma"].shape
@@ -58,6 +57,6 @@ def run(cfg, gamma, sigma, mode=0, elastic=None, min_rates=None, e_fixed=None, w
                       warm_p=ia["warm_p"].ctypes.data if "warm_p" in ia else None)
     bo = _abi.BatchOut(**{k: v.ctypes.data for k, v in oa.items()})
     rc = lib().hcran_emu_solve(C.byref(prob), C.byref(bi), C.byref(bo), mode, 0, B,
-                               1 if dense_off else 0, 1 if engine else 0)
+                               1 if dense_off else 0)
     assert rc == 0
     return oa

@@ -23,13 +23,12 @@ def _check_dinkelbach(g, out, idx, skip=None):
             if not g["near_tie"][i] and not (skip is not None and skip[i]) and not _ok(out, g, j, i)]
 
 
-@pytest.mark.parametrize("engine", [True, False], ids=["smem-engine", "global-engine"])
 @pytest.mark.parametrize("name", ["c0", "c1"])
-def test_emu_default_mode(golden, devmodel, name, engine):
+def test_emu_default_mode(golden, devmodel, name):
     g, dm = golden(name), devmodel(name)
     idx = np.arange(len(g["draw"]))
     b = workload_batch(name, g["draw"][idx])
-    out = runner.run(b.cfg, b.gamma, b.sigma, mode=0, engine=engine)
+    out = runner.run(b.cfg, b.gamma, b.sigma, mode=0)
     fs = dm["floor_sensitive"] if dm is not None else None
     assert _check_dinkelbach(g, out, idx, fs) == []
     if dm is not None:
@@ -48,14 +47,13 @@ def test_emu_exact_mode(golden, name):
     assert _check_dinkelbach(g, out, idx) == []
 
 
-@pytest.mark.parametrize("engine", [True, False], ids=["smem-engine", "global-engine"])
-def test_emu_fixed_e_golden(golden, devmodel, engine):
+def test_emu_fixed_e_golden(golden, devmodel):
     g, dm = golden("c4"), devmodel("c4")
     ref = g if dm is None else dm
     idx = np.arange(len(g["draw"]))
     b = workload_batch("c4", g["draw"][idx])
     out = runner.run(b.cfg, b.gamma, b.sigma, mode=1, elastic=b.elastic, min_rates=b.min_rates,
-                     e_fixed=b.e_fixed, engine=engine)
+                     e_fixed=b.e_fixed)
     for j in idx:
         assert _ok(out, ref, j, j, key="objective"), j
 

@@ -4,8 +4,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1803_07772_b200 import build as B, solver
 lib_path = os.path.join(ROOT, 'tools', 'libhcran_prof.so')
-if not os.path.exists(lib_path):
-    cmd = [B.nvcc()] + B.NVCC_FLAGS + ['-DHCRAN_PROFILE', '-DHCRAN_NO_CLUSTER', '-I' + os.path.join(ROOT, 'include'), '-o', lib_path] + B.SOURCES
+if not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(B.LIB):
+    cmd = [B.nvcc()] + B.NVCC_FLAGS + ['-DHCRAN_PROFILE', '-I' + os.path.join(ROOT, 'include'), '-o', lib_path] + B.SOURCES
     subprocess.run(cmd, check=True, capture_output=True)
 solver.LIB_PATH = lib_path
 lib = solver.library()
@@ -20,13 +20,14 @@ solve_batch(b.cfg, b.gamma, b.sigma)
 lib.hcran_b200_phase_cycles(out, 1)
 o = solve_batch(b.cfg, b.gamma, b.sigma)
 lib.hcran_b200_phase_cycles(out, 0)
-names = {0: 'sw:totals+full', 1: 'sw:decode pass', 2: 'sw:utot', 3: 'sw:psi_cross+pairs', 4: 'sw:num/den', 5: 'sw:X1 partials+exchange',
-         6: 'sw:bisection', 7: 'sw:closed form', 8: 'sw:X3 exchange', 10: 'round_start', 11: 'round_end', 12: 'run:build_seats',
+# thread 0 (warp 0) clock per phase; marks 1-5 are warp 0's own subcarriers
+names = {0: 'sw:products', 1: 'an:tables+full+utot', 2: 'an:columns (psi, own)', 3: 'an:dense family',
+         4: 'an:num/den', 24: 'sw:analyze tail',
+         25: 'sw:dense update', 26: 'sw:budget multiplier', 7: 'sw:closed form+zeta', 8: 'sw:convergence',
+         10: 'round_start', 11: 'round end (surrogate, stops)',
          16: 'inner:setup', 17: 'inner:rounds', 18: 'inner:repair', 19: 'inner:feasible',
-         20: 'g:totals+full', 21: 'g:decode pass', 22: 'g:utot+psi_cross', 23: 'g:dense terms+hf',
-         24: 'g:num/den', 25: 'g:dense update', 26: 'g:bisection',
          27: 'repair:prune+rescale', 28: 'repair:trim', 29: 'repair:boost', 30: 'repair:sic_cleanup', 31: 'repair:final rates'}
-tot = sum(out[i] for i in list(range(0, 9)) + list(range(20, 27))) or 1
+tot = sum(out[i] for i in (0, 1, 2, 3, 4, 24, 25, 26, 7, 8)) or 1
 print('sweeps', int(o['sweeps'].sum().item()), 'instances', nb)
 for i in range(32):
     if out[i]:
