@@ -39,7 +39,11 @@ struct Work {
   double *s_plin, *s_logplin, *s_num, *s_den, *s_psis, *s_cross, *s_inv, *s_rhat, *s_dlog,
       *s_beta, *s_dsA, *s_dsB, *s_nsS, *s_nsW, *s_dagg, *s_aagg, *s_pround,
       *s_mask,   // s_mask: the seat's per-cell power cap (mask), set with the seating
-      *s_alpha;  // the seat's bound slope (per round)
+      *s_alpha,  // the seat's bound slope (per round)
+      *s_p,      // the seat's power (mirrors p at its cell during the rounds)
+      *s_g;      // the seat cell's gain (static per seating)
+  int32_t* s_cell;  // the seat's cell index (static per seating)
+  uint8_t* s_rk;    // the seat's decode rank (static per seating)
   uint8_t* s_user;
   // pairs [MN * NPAIR]
   double *pr_zt, *pr_step, *pr_gconst, *pr_gval, *pr_brk, *pr_slack;
@@ -154,6 +158,7 @@ struct Work {
     HC_D(s_cross, S); HC_D(s_inv, S); HC_D(s_rhat, S); HC_D(s_dlog, S); HC_D(s_beta, S);
     HC_D(s_dsA, S); HC_D(s_dsB, S); HC_D(s_nsS, S); HC_D(s_nsW, S); HC_D(s_dagg, S);
     HC_D(s_aagg, S); HC_D(s_pround, S); HC_D(s_mask, S); HC_D(s_alpha, S);
+    HC_D(s_p, S); HC_D(s_g, S); HC_I(s_cell, S); HC_B(s_rk, S);
     HC_B(s_user, S);
     HC_D(pr_zt, PP); HC_D(pr_step, PP); HC_D(pr_gconst, PP); HC_D(pr_gval, PP);
     HC_D(pr_brk, PP); HC_D(pr_slack, PP);

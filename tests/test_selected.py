@@ -39,7 +39,7 @@ def _compare(name, g, out):
     return bad
 
 
-@pytest.mark.parametrize("name", ["c1"])
+@pytest.mark.parametrize("name", ["c1", "c2"])
 def test_selected_host_build(selected, name):
     from emu import runner
     from paper_1803_07772_b200.scenarios import workload_batch
