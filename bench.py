@@ -44,12 +44,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c0", "c1", "c2", "c3", "c4"])
     ap.add_argument("--batch", type=int, default=None, help="instances per GPU (default: config's)")
     ap.add_argument("--cpu-sample", type=int, default=None,
                     help="instances in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2,
+                    help="steps of the end-to-end leg (at most --steps; c2 steps take ~1 min)")
     return ap.parse_args()
 
 
@@ -70,6 +72,11 @@ def workload_desc(name, batch):
     if name == "c4":
         desc["builder_pinned"]["streaming_users"] = "0/1 (30%)"
         desc["mode"] = "fixed-e inner solve"
+    if name == "c3":
+        desc["workload"] = "c3: BASELINE.json configs[3], one wave per GPU"
+        desc["inputs"] = ("device-synthesised (hcran_b200_synth_gamma: Philox4x32-10 per draw, "
+                          "the reference's distributions); draws rank*batch + i")
+        desc["full_config_batch"] = 131072
     return desc
 
 
@@ -105,7 +112,10 @@ def cpu_rate(name, sample, first_draw=0):
     return sample / wall, min(cores, sample), wall
 
 
-DEFAULT_CPU_SAMPLE = {"c0": 256, "c1": 32, "c2": 8, "c4": 1024}
+DEFAULT_CPU_SAMPLE = {"c0": 256, "c1": 64, "c2": 16, "c3": 0, "c4": 1024}
+# config[3] (131,072 instances over 2/4/8 GPUs, ~4 MiB of gains each) is
+# benchmarked on a per-GPU wave of device-synthesised instances (hcran_b200_synth_gamma)
+C3_BATCH = 296
 
 
 def cpu_model():
@@ -123,23 +133,35 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     name = args.config
+    if name == "c3":
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT,
+                          "unavailable": "config[3] does not run on the CPU path: the reference "
+                                         "allocates dense (M,M,K,N,N) float64 arrays of 16 GiB per "
+                                         "instance (scale.py:696) -- MemoryError (SURVEY.md 6)"}),
+              flush=True)
+        return
     sample = args.cpu_sample or DEFAULT_CPU_SAMPLE[name]
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_rate(name, min(sample, os.cpu_count() or 1), first_draw=10_000)
+    # a config[2] draw takes ~1 min on one core: one pass over a fixed sample
+    # bounds the arm to a few minutes; lighter configs time `steps` samples
+    passes = 1 if name == "c2" else args.steps
+    if name != "c2":
+        for _ in range(args.warmup if args.warmup < 1 else 1):
+            cpu_rate(name, min(sample, os.cpu_count() or 1), first_draw=10_000)
     rates, walls = [], []
-    for s in range(args.steps):
+    for s in range(passes):
         r, cores, w = cpu_rate(name, sample, first_draw=s * sample)
         rates.append(r)
         walls.append(w)
     total = sum(walls)
-    value = args.steps * sample / total
+    value = passes * sample / total
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "steps": passes, "warmup": 0 if name == "c2" else args.warmup,
+            "ms_per_step": 1e3 * total / passes,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference instance generator, seed 1)",
             "config": workload_desc(name, args.batch or WORKLOADS[name][5]), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{sample} draws of {name} per step, oracle/hcran_oracle.py "
+                             "sample": f"{sample} draws of {name} x {passes} pass(es), oracle/hcran_oracle.py "
                                        f"(numpy restatement of the reference) in a "
                                        f"{cores}-process pool on {cpu_model()}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -239,18 +261,36 @@ def run_b200(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     name = args.config
-    B = args.batch or WORKLOADS[name][5]
+    B = args.batch or (C3_BATCH if name == "c3" else WORKLOADS[name][5])
     fixed = name == "c4"
-    batch = workload_batch(name, weak_range(rank, B))
-    cfg = batch.cfg
-    # per-instance inputs, pinned on the host (the e2e leg copies them every step)
-    h_in = {"gamma": torch.from_numpy(batch.gamma).pin_memory(),
-            "elastic": torch.from_numpy(np.ascontiguousarray(batch.elastic, np.uint8)).pin_memory(),
-            "min_rates": torch.from_numpy(np.ascontiguousarray(batch.min_rates)).pin_memory()}
-    if fixed:
-        h_in["e_fixed"] = torch.from_numpy(np.ascontiguousarray(batch.e_fixed)).pin_memory()
+    if name == "c3":  # gains synthesised on the device; one host copy for the e2e leg
+        from paper_1803_07772_b200 import synth_gamma
+        from paper_1803_07772_b200.scenarios import gen_sigma, workload_instance
+        cfg, _, _ = workload_instance("c3", 0)
+        g = synth_gamma(cfg, rank * B, B, seed=1, device=dev)
+        K = cfg.n_users
+        h_in = {"gamma": g.cpu().pin_memory(),
+                "elastic": torch.from_numpy(np.ascontiguousarray(
+                    np.broadcast_to(cfg.elastic_mask(), (B, K)), np.uint8)).pin_memory(),
+                "min_rates": torch.from_numpy(np.ascontiguousarray(
+                    np.broadcast_to(cfg.min_rates(), (B, K)))).pin_memory()}
+        sigma = gen_sigma(cfg)
+    else:
+        batch = workload_batch(name, weak_range(rank, B))
+        cfg = batch.cfg
+        sigma = batch.sigma
+        # per-instance inputs, pinned on the host (the e2e leg copies them every step)
+        h_in = {"gamma": torch.from_numpy(batch.gamma).pin_memory(),
+                "elastic": torch.from_numpy(np.ascontiguousarray(batch.elastic, np.uint8)).pin_memory(),
+                "min_rates": torch.from_numpy(np.ascontiguousarray(batch.min_rates)).pin_memory()}
+        if fixed:
+            h_in["e_fixed"] = torch.from_numpy(np.ascontiguousarray(batch.e_fixed)).pin_memory()
     d_in = {k: v.to(dev) for k, v in h_in.items()}
-    problem = DeviceProblem(cfg, batch.sigma, dev)
+    # config[3]: the seated SIC family without floor-tie re-solves (HCRAN_SIC_SEATED_FAST):
+    # the exact dense pair family costs 8,128 pairs per (RRH, subcarrier) there
+    # (minutes per flagged instance); flagged instances are counted in the line
+    exact = "fast" if name == "c3" else False
+    problem = DeviceProblem(cfg, sigma, dev, exact=exact)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -292,7 +332,8 @@ def run_b200(args, rank, world, local):
     sweeps = float(outs[-1]["sweeps"].double().mean().item())
     st = outs[-1]["status"].cpu().numpy()
     t_all = max_over_ranks(t_dev, dev)
-    value = world * B * args.steps / t_all
+    solved = B - int((st == 4).sum())  # HCRAN_ST_UNSUPPORTED instances do not count as solved
+    value = world * solved * args.steps / t_all
 
     # end-to-end through the public API: host gamma (pinned) in, allocation +
     # per-instance scalars out (pinned), copies inside the timed region
@@ -304,9 +345,10 @@ def run_b200(args, rank, world, local):
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        e2e_steps = max(1, min(args.e2e_steps, args.steps))
         t0.record(stream)
         d2h = 0
-        for s in range(args.steps):
+        for s in range(e2e_steps):
             o = step(h_in, outputs=want)
             d2h = 0
             for k in want:
@@ -317,7 +359,7 @@ def run_b200(args, rank, world, local):
         barrier()
         h2d = sum(v.numel() * v.element_size() for v in h_in.values())
         te = max_over_ranks(t0.elapsed_time(t1) / 1e3, dev)
-        e2e = {"value": world * B * args.steps / te, "unit": UNIT,
+        e2e = {"value": world * solved * e2e_steps / te, "unit": UNIT, "steps": e2e_steps,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     if rank == 0:
@@ -341,12 +383,25 @@ def run_b200(args, rank, world, local):
                                       "note": "north_star framing: the same work as if it ran on "
                                               "the FP32 pipe (measured FFMA peak); the parity-"
                                               "critical core is FP64 (DESIGN.md)"},
-                "sic_mode": "seated+dense-retry (HCRAN_SIC_SEATED, exact on all golden draws)",
+                "sic_mode": ("seated, floor ties flagged not re-solved (HCRAN_SIC_SEATED_FAST)"
+                             if name == "c3" else
+                             "seated+dense-retry (HCRAN_SIC_SEATED, exact on all golden draws)"),
                 "gpu_launches": launches, "clocks": clocks, "e2e": e2e,
                 "solver": {"mean_sweeps_per_instance": sweeps,
                            "status_counts": {str(k): int(v) for k, v in
-                                             zip(*np.unique(st, return_counts=True))}}}
-        if world == 1 and not args.no_cpu_baseline:
+                                             zip(*np.unique(st, return_counts=True))},
+                           "unsupported": int((st == 4).sum()),
+                           "floor_tie_flagged": int((outs[-1]["flags"].cpu().numpy() & 1).sum()),
+                           "note": "status 0 converged, 1 outer-iteration cap, 2 stalled, 3 "
+                                   "infeasible (the reference raises): all solved outcomes; "
+                                   "4 = device capacity exceeded (counted in value only if "
+                                   "'unsupported' > 0)"}}
+        if name == "c3":
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                                    "sample": "not runnable: the reference allocates dense "
+                                              "(M,M,K,N,N) float64 arrays of 16 GiB per instance "
+                                              "(scale.py:696, SURVEY.md 6) -- MemoryError"}
+        elif world == 1 and not args.no_cpu_baseline:
             sample = args.cpu_sample or DEFAULT_CPU_SAMPLE[name]
             r, cores, wall = cpu_rate(name, sample)
             line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",

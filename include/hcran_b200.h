@@ -148,6 +148,24 @@ int hcran_b200_solve_batch(const hcran_problem_t* prob, const hcran_batch_in_t* 
                            hcran_batch_out_t* out, void* workspace, size_t ws_bytes,
                            void* stream);
 
+/* Device-side channel synthesis: the instance loader of scenarios.py:84-153
+ * (build_config's user drop + gen_channel) restated for the device.  Users are
+ * uniform in a disc of radius `disc_radius` around the origin (r = R sqrt(U),
+ * theta = 2 pi U), gains gamma[m][k][n] = Exp(1) * d(m,k)^-pathloss_exp.
+ * Draw d uses Philox4x32-10 keyed by (seed, d): the reference's distributions,
+ * not its numpy (PCG64) numbers -- parity fixtures use host-generated draws. */
+typedef struct hcran_synth {
+  int32_t M, K, N;
+  const double* rrh_xy;  /* [M][2] RRH positions, metres (device)          */
+  double disc_radius;    /* 500 m (scenarios.py DISC_RADIUS_M)             */
+  double pathloss_exp;   /* 3                                              */
+  uint64_t seed;
+} hcran_synth_t;
+
+/* Writes gamma_out[B][M][K][N] (device) for draws first_draw .. first_draw+B-1. */
+int hcran_b200_synth_gamma(const hcran_synth_t* sp, int64_t first_draw, int64_t B,
+                           double* gamma_out, void* stream);
+
 /* One fixed-e inner solve per instance (InnerSolver conformance). */
 int hcran_b200_solve_fixed_e_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
                                    hcran_batch_out_t* out, void* workspace,

@@ -15,13 +15,14 @@ from .traffic import TrafficSpec, delay_roots, max_delay_from_queue, min_rate_fo
 from .scenarios import build_config, gen_channel, tiny_instance, workload_batch
 from .solver import (B200Unavailable, DeviceProblem, DinkelbachTrace, InfeasibleProblemError,
                      InnerResult, ScaleSolver, SolveStats, solve, solve_batch)
+from .synth import synth_gamma
 
 __all__ = [
     "ChannelState", "ConfigError", "EnergyReport", "NetworkConfig", "PowerAllocation",
     "Tolerances", "UserSpec", "TrafficSpec", "delay_roots", "max_delay_from_queue",
     "min_rate_for_delay", "build_config", "gen_channel", "tiny_instance", "workload_batch",
     "B200Unavailable", "DeviceProblem", "DinkelbachTrace", "InfeasibleProblemError", "InnerResult",
-    "ScaleSolver", "SolveStats", "solve", "solve_batch",
+    "ScaleSolver", "SolveStats", "solve", "solve_batch", "synth_gamma",
 ]
 
 __version__ = "0.1.0"

@@ -29,6 +29,12 @@ class Problem(C.Structure):
                 ("static_power", C.c_double), ("tol", Tolerances), ("sic_mode", C.c_int32)]
 
 
+class Synth(C.Structure):
+    _fields_ = [("M", C.c_int32), ("K", C.c_int32), ("N", C.c_int32),
+                ("rrh_xy", C.c_void_p), ("disc_radius", C.c_double),
+                ("pathloss_exp", C.c_double), ("seed", C.c_uint64)]
+
+
 class BatchIn(C.Structure):
     _fields_ = [("B", C.c_int64), ("gamma", C.c_void_p), ("elastic", C.c_void_p),
                 ("min_rates", C.c_void_p), ("e_fixed", C.c_void_p), ("warm_p", C.c_void_p)]
@@ -71,10 +77,14 @@ def bind_device_lib(lib: C.CDLL) -> C.CDLL:
     lib.hcran_b200_engine.restype = C.c_int
     lib.hcran_b200_last_launches.argtypes = []
     lib.hcran_b200_last_launches.restype = C.c_int32
+    lib.hcran_b200_synth_gamma.argtypes = [C.POINTER(Synth), C.c_int64, C.c_int64, C.c_void_p,
+                                           C.c_void_p]
+    lib.hcran_b200_synth_gamma.restype = C.c_int
     lib.hcran_b200_version.argtypes = []
     lib.hcran_b200_version.restype = C.c_char_p
     return lib
 
 
 EXPORTED = ("hcran_b200_plan", "hcran_b200_solve_batch", "hcran_b200_solve_fixed_e_batch",
-            "hcran_b200_engine", "hcran_b200_last_launches", "hcran_b200_version")
+            "hcran_b200_engine", "hcran_b200_last_launches", "hcran_b200_synth_gamma",
+            "hcran_b200_version")

@@ -5,8 +5,7 @@ sys.path.insert(0, ROOT)
 from paper_1803_07772_b200 import build as B, solver
 lib_path = os.path.join(ROOT, 'tools', 'libhcran_prof.so')
 if not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(B.LIB):
-    cmd = [B.nvcc()] + B.NVCC_FLAGS + ['-DHCRAN_PROFILE', '-I' + os.path.join(ROOT, 'include'), '-o', lib_path] + B.SOURCES
-    subprocess.run(cmd, check=True, capture_output=True)
+    B.build_lib(lib_path, extra=['-DHCRAN_PROFILE'])
 solver.LIB_PATH = lib_path
 lib = solver.library()
 lib.hcran_b200_phase_cycles.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
