@@ -130,6 +130,12 @@ typedef struct hcran_batch_out {
   int32_t* sweeps_trace; /* [B][outer_max] sweeps per outer iteration          */
   uint8_t* flags;        /* [B] HCRAN_FLAG_* diagnostics                        */
   double* work;          /* [B] algorithmic FP64 work, flop-equivalents */
+  /* SolveStats of the last inner solve (scale.py:405-418) */
+  double* round_obj;     /* [B][tol.s_max] surrogate objective per SCA round (nan-padded) */
+  double* fp_residual;   /* [B] fixed-point residual |p - update(p)| / p_max at exit;
+                            computed only when this pointer is set (one extra sweep) */
+  double* max_dual;      /* [B] largest multiplier entry                         */
+  int32_t* floor_hits;   /* [B] seated cells with den <= 1e-12 den_scale and num > 0 */
 } hcran_batch_out_t;
 
 /* flags: a seat met num == 0 with den <= 0 in the seated-pair SIC model, i.e.
@@ -147,6 +153,15 @@ int hcran_b200_plan(const hcran_problem_t* prob, int64_t B, int device,
 int hcran_b200_solve_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
                            hcran_batch_out_t* out, void* workspace, size_t ws_bytes,
                            void* stream);
+
+/* Energy report of given allocations (warm_p, [B][M][K][N]): sum rate, total
+ * power, EE, objective at e_fixed (or 0), feasibility, rho / a -- the
+ * reference's model.energy_efficiency / check_feasibility / derive_binaries
+ * (model.py:338-341, 404-521).  Used by the host-driven Dinkelbach loop over
+ * an arbitrary InnerSolver (dinkelbach.py:65-112). */
+int hcran_b200_report_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
+                            hcran_batch_out_t* out, void* workspace, size_t ws_bytes,
+                            void* stream);
 
 /* Device-side channel synthesis: the instance loader of scenarios.py:84-153
  * (build_config's user drop + gen_channel) restated for the device.  Users are

@@ -14,7 +14,7 @@ from .model import (ChannelState, ConfigError, EnergyReport, NetworkConfig,
 from .traffic import TrafficSpec, delay_roots, max_delay_from_queue, min_rate_for_delay
 from .scenarios import build_config, gen_channel, tiny_instance, workload_batch
 from .solver import (B200Unavailable, DeviceProblem, DinkelbachTrace, InfeasibleProblemError,
-                     InnerResult, ScaleSolver, SolveStats, solve, solve_batch)
+                     InnerResult, ScaleSolver, SolveStats, energy_report, solve, solve_batch)
 from .synth import synth_gamma
 
 __all__ = [
@@ -22,7 +22,7 @@ __all__ = [
     "Tolerances", "UserSpec", "TrafficSpec", "delay_roots", "max_delay_from_queue",
     "min_rate_for_delay", "build_config", "gen_channel", "tiny_instance", "workload_batch",
     "B200Unavailable", "DeviceProblem", "DinkelbachTrace", "InfeasibleProblemError", "InnerResult",
-    "ScaleSolver", "SolveStats", "solve", "solve_batch", "synth_gamma",
+    "ScaleSolver", "SolveStats", "energy_report", "solve", "solve_batch", "synth_gamma",
 ]
 
 __version__ = "0.1.0"

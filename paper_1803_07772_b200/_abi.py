@@ -51,6 +51,8 @@ OUT_FIELDS = [
     ("e_trace", "f8", "T"), ("surplus_trace", "f8", "T"),
     ("rounds_trace", "i4", "T"), ("sweeps_trace", "i4", "T"),
     ("flags", "u1", ""), ("work", "f8", ""),
+    ("round_obj", "f8", "S"), ("fp_residual", "f8", ""), ("max_dual", "f8", ""),
+    ("floor_hits", "i4", ""),
 ]
 
 
@@ -67,7 +69,8 @@ def bind_device_lib(lib: C.CDLL) -> C.CDLL:
     lib.hcran_b200_plan.argtypes = [C.POINTER(Problem), C.c_int64, C.c_int,
                                     C.POINTER(C.c_int32), C.POINTER(C.c_size_t)]
     lib.hcran_b200_plan.restype = C.c_int
-    for fn in (lib.hcran_b200_solve_batch, lib.hcran_b200_solve_fixed_e_batch):
+    for fn in (lib.hcran_b200_solve_batch, lib.hcran_b200_solve_fixed_e_batch,
+               lib.hcran_b200_report_batch):
         fn.argtypes = [C.POINTER(Problem), C.POINTER(BatchIn), C.POINTER(BatchOut),
                        C.c_void_p, C.c_size_t, C.c_void_p]
         fn.restype = C.c_int
@@ -87,4 +90,5 @@ def bind_device_lib(lib: C.CDLL) -> C.CDLL:
 
 EXPORTED = ("hcran_b200_plan", "hcran_b200_solve_batch", "hcran_b200_solve_fixed_e_batch",
             "hcran_b200_engine", "hcran_b200_last_launches", "hcran_b200_synth_gamma",
+            "hcran_b200_report_batch",
             "hcran_b200_version")

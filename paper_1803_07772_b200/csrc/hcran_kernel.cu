@@ -230,6 +230,8 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   if (rc) return rc;
   if (!in || !out || !workspace || !in->gamma || !in->elastic || !in->min_rates) return HCRAN_E_ARG;
   if (mode == 1 && !in->e_fixed) return HCRAN_E_ARG;
+  if (mode == 2 && !in->warm_p) return HCRAN_E_ARG;
+  if (prob->tol.s_max > RMAX) return HCRAN_E_SIZE;
   if (in->B <= 0) return HCRAN_OK;
   int device = 0;
   cudaGetDevice(&device);
@@ -301,6 +303,12 @@ extern "C" int hcran_b200_solve_fixed_e_batch(const hcran_problem_t* prob,
                                               const hcran_batch_in_t* in, hcran_batch_out_t* out,
                                               void* workspace, size_t ws_bytes, void* stream) {
   return launch(prob, in, out, workspace, ws_bytes, stream, 1);
+}
+
+extern "C" int hcran_b200_report_batch(const hcran_problem_t* prob, const hcran_batch_in_t* in,
+                                       hcran_batch_out_t* out, void* workspace, size_t ws_bytes,
+                                       void* stream) {
+  return launch(prob, in, out, workspace, ws_bytes, stream, 2);
 }
 
 extern "C" int32_t hcran_b200_last_launches(void) { return g_last_launches; }

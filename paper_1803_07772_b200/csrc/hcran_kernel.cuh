@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(NT, 1)
     if (v.flag_in && !v.flag_in[b]) continue;
     S.load_instance(b);
     if (mode == 0) S.dinkelbach(b);
-    else S.fixed_e(b);
+    else if (mode == 1) S.fixed_e(b);
+    else S.report(b);
     ex.sync();
   }
 }

@@ -21,6 +21,7 @@ constexpr uint8_t NOSLOT = 0xFF;
 // sparse rows, live only for non-exclusive seatings
 constexpr int TQMAX = 64;    // materialised tuple rows (theta'), per inner solve
 constexpr int THMAX = 1024;  // cross-head seat pairs of one user (theta)
+constexpr int RMAX = 64;     // SCA rounds per inner solve (Tolerances.s_max <= RMAX)
 
 struct Work {
   // dense [C], reference order [m][k][n]
@@ -76,6 +77,7 @@ struct Work {
   double *th_val, *th_step, *th_slack;             // [THMAX]
   double *s_ppair, *s_ptup;                        // [S] per-seat pair / tuple pressure
   double* pbest;                                   // [C] multistart: best start's end point
+  double *robj, *robj_best;                        // [RMAX] round objectives (current / accepted start)
 
   double* wleaf;    // [nw][wlstride]: leaf sums of the warp-parallel pairwise sums
   int32_t* wleafi;  // [nw][wlstride]: their offsets (PwCache)
@@ -179,6 +181,7 @@ struct Work {
     HC_D(th_slack, THMAX);
     HC_D(s_ppair, S); HC_D(s_ptup, S);
     HC_D(pbest, C <= 4096 ? C : 1);
+    HC_D(robj, RMAX); HC_D(robj_best, RMAX);
     if (dense) {
       const size_t PD = MN * (size_t(K) * (K - 1) / 2);
       HC_D(cx, C); HC_D(cxl, C); HC_D(dA, C); HC_D(dB, C); HC_D(nS, C); HC_D(nW, C);

@@ -66,10 +66,10 @@ def instance_arrays(cfgs_or_cfg, gamma: np.ndarray, elastic=None, min_rates=None
     return out
 
 
-def out_arrays(B: int, M: int, K: int, N: int, T: int, want=None) -> dict:
+def out_arrays(B: int, M: int, K: int, N: int, T: int, want=None, S: int = 20) -> dict:
     arrs = {}
     for name, dt, kind in _abi.OUT_FIELDS:
         if want is not None and name not in want:
             continue
-        arrs[name] = np.zeros(_abi.out_shape(kind, B, M, K, N, T), dtype=dt)
+        arrs[name] = np.zeros(_abi.out_shape(kind, B, M, K, N, T, S), dtype=dt)
     return arrs

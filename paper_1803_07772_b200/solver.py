@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -104,7 +105,8 @@ def solve_batch(cfg, gamma, sigma=None, elastic=None, min_rates=None, *, mode="d
     gamma      (B, M, K, N) float64 channel gains: numpy (copied in) or a CUDA tensor
     sigma      (M, K, N) noise powers (default: the config's flat noise floor)
     elastic    (B, K) bool / min_rates (B, K): per-instance user classes (default: cfg's)
-    mode       "dinkelbach" (full solve) or "fixed_e" (one inner solve per instance)
+    mode       "dinkelbach" (full solve), "fixed_e" (one inner solve per instance) or
+               "report" (energy report of the allocations in warm_p at e_fixed)
     exact      False (default): seated SIC family, inner solves that meet a floor tie
                are redone with the dense family (HCRAN_SIC_SEATED); True: dense family
                everywhere (HCRAN_SIC_DENSE); "fast": seated family only, floor ties not
@@ -144,7 +146,7 @@ def _solve_batch_on(torch, lib, dev, s, cfg, gamma, sigma, elastic, min_rates, m
     el = _on_device(elastic, torch.uint8, dev)
     mr = _on_device(min_rates, torch.float64, dev)
     ef = None
-    if mode == "fixed_e":
+    if mode in ("fixed_e", "report"):
         if not isinstance(e_fixed, torch.Tensor):
             e_fixed = np.broadcast_to(e_fixed, (B,))
         ef = _on_device(e_fixed, torch.float64, dev)
@@ -168,7 +170,8 @@ def _solve_batch_on(torch, lib, dev, s, cfg, gamma, sigma, elastic, min_rates, m
         raise ValueError(f"hcran_b200_plan: {_abi.ERRORS.get(rc, rc)}")
     if workspace is None or workspace.numel() < wsb.value:
         workspace = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
-    fn = lib.hcran_b200_solve_batch if mode == "dinkelbach" else lib.hcran_b200_solve_fixed_e_batch
+    fn = {"dinkelbach": lib.hcran_b200_solve_batch, "fixed_e": lib.hcran_b200_solve_fixed_e_batch,
+          "report": lib.hcran_b200_report_batch}[mode]
     rc = fn(C.byref(prob.struct), C.byref(bi), C.byref(bo), workspace.data_ptr(), wsb.value,
             s.cuda_stream)
     if rc:
@@ -184,16 +187,25 @@ def _solve_batch_on(torch, lib, dev, s, cfg, gamma, sigma, elastic, min_rates, m
 
 @dataclass
 class SolveStats:
-    """Mirrors scale.SolveStats (scale.py:405-418) for the fields the device reports."""
+    """scale.SolveStats (scale.py:405-418).  Every field is reported by the
+    device for the inner solve; `trace` (per-sweep records of
+    collect_trace=True) stays empty: the sweeps never leave the device.
+    `denominator_floor_hits` counts seated cells (unseated cells are pinned at
+    p_floor and their denominators are floor-level noise)."""
     status: str = "ok"
     rounds: int = 0
     total_sweeps: int = 0
+    round_objectives: list = field(default_factory=list)
     true_objective: float = float("nan")
     used_warm_start: bool = False
+    denominator_floor_hits: int = 0
+    max_dual: float = 0.0
+    fixed_point_residual: float = float("nan")
     infeasible_reason: str | None = None
-    budget_evals: int = 0
+    wall_time: float = 0.0
+    trace: list = field(default_factory=list)
+    budget_evals: int = 0   # device counters (no reference counterpart)
     flags: int = 0
-    round_objectives: list = field(default_factory=list)
 
 
 @dataclass
@@ -231,54 +243,123 @@ def _host(outs: dict) -> dict:
 
 
 class ScaleSolver:
-    """B200 inner solver with the reference's InnerSolver interface.
+    """B200 inner solver with the reference's InnerSolver interface
+    (scale.py:489-551, dinkelbach.py:28-33).
 
-    `solve_fixed_e` runs one fixed-e solve (scale.py:506-551) on the device;
-    `solve(ch, cfg, ScaleSolver())` runs the whole Dinkelbach loop on the
-    device.  Constructor knobs of the reference (workers, collect_trace, gains,
-    damping, min_sweeps, multistart_cells) are accepted for drop-in
-    compatibility; only the reference defaults are implemented on device."""
+    `solve_fixed_e` runs one fixed-e solve on the device and returns an
+    `InnerResult` with the reference's `SolveStats`; `solve(ch, cfg,
+    ScaleSolver())` runs the whole Dinkelbach loop on the device.  The
+    reference's constructor knobs are accepted: `workers` (the reference's
+    serial == parallel contract holds trivially) and `collect_trace` (no
+    per-sweep records) change nothing; the step gains, damping, min_sweeps and
+    multistart_cells are compiled into the device solver at the reference's
+    defaults, so other values raise NotImplementedError."""
 
     def __init__(self, workers: int = 1, collect_trace: bool = False,
                  gains=(0.6, 0.8, 0.6, 0.6, 0.6), damping: float = 1.0, min_sweeps: int = 8,
                  multistart_cells: int = 16, device=None):
-        if tuple(gains) != (0.6, 0.8, 0.6, 0.6, 0.6) or damping != 1.0 or min_sweeps != 8:
+        if (tuple(gains) != (0.6, 0.8, 0.6, 0.6, 0.6) or damping != 1.0 or min_sweeps != 8
+                or multistart_cells != 16):
             raise NotImplementedError("the B200 solver implements the reference defaults only")
+        self.workers = workers
+        self.collect_trace = collect_trace
         self.device = device
 
     def solve_fixed_e(self, ch, cfg, e: float, warm_start: PowerAllocation | None = None):
         if e < 0:
             raise ValueError("the efficiency parameter must be non-negative")
+        t0 = time.perf_counter()
         warm = None if warm_start is None else np.asarray(warm_start.p, np.float64)[None]
         o = _host(solve_batch(cfg, np.asarray(ch.gamma)[None], np.asarray(ch.sigma),
                               mode="fixed_e", e_fixed=float(e), warm_p=warm,
                               device=self.device))
         st = int(o["status"][0])
+        if st == 4:
+            raise NotImplementedError("seating beyond the device's per-column capacity "
+                                      "(HCRAN_ST_UNSUPPORTED)")
         status = _abi.HCRAN_ST_FIXED.get(st, "infeasible")
+        ro = o["round_obj"][0]
         stats = SolveStats(status=status, rounds=int(o["rounds"][0]),
                            total_sweeps=int(o["sweeps"][0]),
+                           round_objectives=[float(x) for x in ro[~np.isnan(ro)]],
                            used_warm_start=warm_start is not None,
+                           denominator_floor_hits=int(o["floor_hits"][0]),
+                           max_dual=float(o["max_dual"][0]),
+                           fixed_point_residual=float(o["fp_residual"][0]),
                            budget_evals=int(o["bisect_evals"][0]), flags=int(o["flags"][0]))
-        if st == 4:
-            raise NotImplementedError("non-exclusive seating (products-active families)")
         alloc = PowerAllocation(p=o["p"][0].copy())
         if status == "ok":
             alloc.rho, alloc.a = o["rho"][0].copy(), o["a"][0].copy()
             stats.true_objective = float(o["objective"][0])
         else:
             stats.infeasible_reason = "repair could not meet the streaming rates"
+        stats.wall_time = time.perf_counter() - t0
         return InnerResult(alloc, status, stats)
 
 
+def energy_report(ch, cfg, allocations, e: float = 0.0, device=None) -> dict:
+    """(sum_rate, total_power, ee, objective at e, feasible, rho, a) of given
+    allocations, computed on the device (hcran_b200_report_batch): the
+    reference's model.energy_efficiency / check_feasibility / derive_binaries."""
+    p = np.asarray(allocations, np.float64)
+    if p.ndim == 3:
+        p = p[None]
+    g = np.broadcast_to(np.asarray(ch.gamma), p.shape)
+    return _host(solve_batch(cfg, np.ascontiguousarray(g), np.asarray(ch.sigma), mode="report",
+                             e_fixed=float(e), warm_p=p, device=device,
+                             outputs=["sum_rate", "total_power", "ee", "objective", "feasible",
+                                      "rho", "a", "status"]))
+
+
 def solve(ch, cfg, inner=None, e0: float = 0.0) -> DinkelbachTrace:
-    """dinkelbach.solve with the outer loop on the device (dinkelbach.py:65-112)."""
-    if inner is not None and not isinstance(inner, ScaleSolver):
-        raise TypeError("the B200 Dinkelbach loop runs on the device with the B200 ScaleSolver")
-    if e0 != 0.0:
-        raise NotImplementedError("the device loop starts from e0 = 0 (the reference default)")
-    dev = inner.device if inner is not None else None
-    o = _host(solve_batch(cfg, np.asarray(ch.gamma)[None], np.asarray(ch.sigma), device=dev))
-    return trace_from_batch(o, 0)
+    """dinkelbach.solve (dinkelbach.py:65-112).
+
+    With the B200 ScaleSolver (or no inner solver) and e0 = 0 the whole outer
+    loop runs on the device in one launch.  Any other InnerSolver (the
+    reference's protocol: `solve_fixed_e(ch, cfg, e, warm_start)` returning
+    `.allocation`, `.status`, `.stats`) is driven by the reference's host loop,
+    with the surplus and EE of each allocation evaluated on the device."""
+    if e0 < 0:
+        raise ValueError("the efficiency parameter must be non-negative")
+    if (inner is None or isinstance(inner, ScaleSolver)) and e0 == 0.0:
+        dev = inner.device if inner is not None else None
+        o = _host(solve_batch(cfg, np.asarray(ch.gamma)[None], np.asarray(ch.sigma), device=dev))
+        return trace_from_batch(o, 0)
+    if inner is None:
+        inner = ScaleSolver()
+    dev = getattr(inner, "device", None)
+    tol = cfg.tolerances
+    tr = DinkelbachTrace()
+    e, warm = e0, None
+    for _ in range(tol.outer_max):
+        result = inner.solve_fixed_e(ch, cfg, e, warm_start=warm)
+        if result.status != "ok":
+            if warm is None:
+                raise InfeasibleProblemError(
+                    "inner solver found no feasible allocation at e="
+                    f"{e:g}: {getattr(result.stats, 'infeasible_reason', None)}")
+            tr.status = "stalled"
+            break
+        warm = result.allocation
+        rep = energy_report(ch, cfg, warm.p, e, device=dev)
+        s = float(rep["objective"][0])  # R - e P (dinkelbach.surplus)
+        tr.iterations.append(DinkelbachIteration(e=e, surplus=s, inner_stats=result.stats))
+        ee = float(rep["ee"][0])
+        if s <= tol.xi:
+            tr.final_e, tr.final_allocation, tr.status = ee, warm, "converged"
+            return tr
+        if ee <= e:
+            tr.status = "stalled"
+            break
+        e = ee
+    else:
+        tr.cap_hit = True
+        tr.status = "cap"
+    if warm is None:
+        raise InfeasibleProblemError("inner solver produced no allocation")
+    tr.final_e = float(energy_report(ch, cfg, warm.p, device=dev)["ee"][0])
+    tr.final_allocation = warm
+    return tr
 
 
 def trace_from_batch(o: dict, b: int) -> DinkelbachTrace:
@@ -286,7 +367,8 @@ def trace_from_batch(o: dict, b: int) -> DinkelbachTrace:
     if st == 3:
         raise InfeasibleProblemError("inner solver found no feasible allocation at e=0")
     if st == 4:
-        raise NotImplementedError("non-exclusive seating (products-active families)")
+        raise NotImplementedError("seating beyond the device's per-column capacity "
+                                  "(HCRAN_ST_UNSUPPORTED)")
     tr = DinkelbachTrace()
     n_it = int(o["outer_iters"][b])
     for i in range(n_it):

@@ -40,7 +40,8 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   for (int64_t b = first; b < first + count && b < in->B; ++b) {
     S.load_instance(b);
     if (mode == 0) S.dinkelbach(b);
-    else S.fixed_e(b);
+    else if (mode == 1) S.fixed_e(b);
+    else S.report(b);
   }
   free(base);
   return 0;

@@ -49,7 +49,7 @@ def run(cfg, gamma, sigma, mode=0, elastic=None, min_rates=None, e_fixed=None, w
     ia = pack.instance_arrays(cfg, gamma, elastic, min_rates, e_fixed, warm_p)
     B, M, K, N = ia["gamma"].shape
     T = cfg.tolerances.outer_max
-    oa = pack.out_arrays(B, M, K, N, T)
+    oa = pack.out_arrays(B, M, K, N, T, S=cfg.tolerances.s_max)
     prob = pack.problem_struct(cfg, {k: v.ctypes.data for k, v in pa.items()}, exact=exact)
     bi = _abi.BatchIn(B=B, gamma=ia["gamma"].ctypes.data, elastic=ia["elastic"].ctypes.data,
                       min_rates=ia["min_rates"].ctypes.data,
