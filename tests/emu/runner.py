@@ -40,7 +40,46 @@ def lib():
                                          C.POINTER(_abi.BatchOut), C.c_int, C.c_int64,
                                          C.c_int64, C.c_int]
         _lib.hcran_emu_solve.restype = C.c_int
+        P = C.POINTER(C.c_double)
+        _lib.hcran_emu_budget.argtypes = [P, P, P, C.c_int, C.c_int, P, P, P,
+                                          C.POINTER(C.c_int)]
+        _lib.hcran_emu_budget.restype = None
+        _lib.hcran_emu_sweep_snapshot.argtypes = [C.POINTER(_abi.Problem), C.POINTER(_abi.BatchIn),
+                                                  P, P, P, P, P, P, P]
+        _lib.hcran_emu_sweep_snapshot.restype = C.c_int
     return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def budget(num, den, mask, budget_, warm):
+    """The device budget multiplier on the reference's (M, K, N) inputs."""
+    num, den, mask = (np.ascontiguousarray(x, np.float64) for x in (num, den, mask))
+    M = num.shape[0]
+    KN = num.size // M
+    b = np.ascontiguousarray(budget_, np.float64)
+    w = np.ascontiguousarray(warm, np.float64)
+    xi = np.zeros(M)
+    ev = (C.c_int * M)()
+    lib().hcran_emu_budget(_dp(num), _dp(den), _dp(mask), M, KN, _dp(b), _dp(w), _dp(xi), ev)
+    return xi, np.array(ev[:])
+
+
+def sweep_snapshot(cfg, gamma, sigma, p0, xi0, zeta0, zeta_t0):
+    """One device sweep from a reference round-start snapshot."""
+    pa = pack.problem_arrays(cfg, sigma)
+    ia = pack.instance_arrays(cfg, gamma[None])
+    prob = pack.problem_struct(cfg, {k: v.ctypes.data for k, v in pa.items()})
+    bi = _abi.BatchIn(B=1, gamma=ia["gamma"].ctypes.data, elastic=ia["elastic"].ctypes.data,
+                      min_rates=ia["min_rates"].ctypes.data, e_fixed=None, warm_p=None)
+    p0, xi0, zeta0 = (np.ascontiguousarray(x, np.float64) for x in (p0, xi0, zeta0))
+    zt = np.ascontiguousarray(zeta_t0, np.float64).copy()
+    p_out, xi_out, z_out = np.zeros_like(p0), np.zeros_like(xi0), np.zeros_like(zeta0)
+    fg = lib().hcran_emu_sweep_snapshot(C.byref(prob), C.byref(bi), _dp(p0), _dp(xi0), _dp(zeta0),
+                                        _dp(zt), _dp(p_out), _dp(xi_out), _dp(z_out))
+    return p_out, xi_out, z_out, zt, bool(fg)
 
 
 def run(cfg, gamma, sigma, mode=0, elastic=None, min_rates=None, e_fixed=None, warm_p=None,
