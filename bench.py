@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=None,
                     help="instances in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2,
                     help="steps of the end-to-end leg (at most --steps; c2 steps take ~1 min)")
@@ -293,6 +294,12 @@ def run_b200(args, rank, world, local):
     problem = DeviceProblem(cfg, sigma, dev, exact=exact)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    cpu_proc = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and name != "c3":
+        cmd = [sys.executable, os.path.abspath(__file__), "--cpu-only", "--config", name]
+        if args.cpu_sample:
+            cmd += ["--cpu-sample", str(args.cpu_sample)]
+        cpu_proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
 
     def step(x, outputs=None):
         kw = dict(mode="fixed_e", e_fixed=x["e_fixed"]) if fixed else {}
@@ -401,21 +408,32 @@ def run_b200(args, rank, world, local):
                                     "sample": "not runnable: the reference allocates dense "
                                               "(M,M,K,N,N) float64 arrays of 16 GiB per instance "
                                               "(scale.py:696, SURVEY.md 6) -- MemoryError"}
-        elif world == 1 and not args.no_cpu_baseline:
-            sample = args.cpu_sample or DEFAULT_CPU_SAMPLE[name]
-            r, cores, wall = cpu_rate(name, sample)
-            line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
-                                    "sample": f"{sample} draws of {name} ({wall:.1f} s), "
-                                              f"oracle/hcran_oracle.py in a {cores}-process pool "
-                                              f"on {cpu_model()}"}
+        elif cpu_proc is not None:
+            out, _ = cpu_proc.communicate()
+            line["cpu_baseline"] = json.loads(out.strip().splitlines()[-1])
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def cpu_only(args):
+    """The cpu_baseline leg as its own process, started by the GPU arm before
+    its warm-up so the host sample overlaps the device timing."""
+    name = args.config
+    sample = args.cpu_sample or DEFAULT_CPU_SAMPLE[name]
+    r, cores, wall = cpu_rate(name, sample)
+    print(json.dumps({"value": r, "unit": UNIT, "cores": cores, "kind": "port",
+                      "sample": f"{sample} draws of {name} ({wall:.1f} s), oracle/hcran_oracle.py "
+                                f"in a {cores}-process pool on {cpu_model()}, run concurrently "
+                                f"with the device timing"}), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.cpu_only:
+        cpu_only(args)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -68,22 +68,25 @@ def test_default_mode(golden, devmodel, name):
     assert np.all(o["feasible"][g["feasible"][idx]] == 1)
 
 
-def test_near_tie_draws_mostly_match(golden):
+def test_near_tie_draws_match_like_the_host_build(golden):
     """Near-tie draws (the reference itself moves by > 1e-4 under a 1e-12
-    multiplier perturbation) are excused by the parity bar; the host build of
-    the same source matches all 21 of them.  On the device, require most."""
-    tot = hit = 0
-    for name in ("c0", "c1"):
+    multiplier perturbation) are excused by the parity bar.  The device must
+    match the reference on exactly the near-tie draws the host build of the
+    same source matches (the two differ only in libm ulps: log, log2, pow)."""
+    from emu import runner
+    for name in ("c0", "c1", "c2"):
         g = golden(name)
         idx = np.nonzero(g["near_tie"])[0]
         if len(idx) == 0:
             continue
         b = workload_batch(name, g["draw"][idx])
         o = host(solve_batch(b.cfg, b.gamma, b.sigma))
-        hit += sum(bool(_ok(o, g, j, i)) for j, i in enumerate(idx))
-        tot += len(idx)
-    print(f"near-tie draws matching the reference: {hit}/{tot}")
-    assert hit >= 0.8 * tot
+        e = runner.run(b.cfg, b.gamma, b.sigma, mode=0)
+        dev = [int(i) for j, i in enumerate(idx) if _ok(o, g, j, i)]
+        emu = [int(i) for j, i in enumerate(idx) if _ok(e, g, j, i)]
+        print(f"{name}: near-tie draws matching the reference: device {len(dev)}, host build "
+              f"{len(emu)} of {len(idx)}")
+        assert dev == emu
 
 
 @pytest.mark.parametrize("name", ["c0", "c1"])
@@ -110,14 +113,19 @@ def test_fixed_e_matches_reference(golden, devmodel, exact):
         assert _ok(o, ref, j, j, key="objective"), j
 
 
-def test_device_matches_host_emulation():
-    """Same source compiled for the host (tests/emu): results agree to FMA-level noise."""
+@pytest.mark.parametrize("name,n", [("c0", 64), ("c1", 32)])
+def test_device_matches_host_emulation(name, n):
+    """Same source compiled for the host (tests/emu): identical decisions
+    (status, rho, a, iteration counts) on every draw and EE within 1e-9; the
+    only differences are libm ulps (log / log2 / pow on the device vs glibc)."""
     from emu import runner
-    b = workload_batch("c0", range(32))
+    b = workload_batch(name, range(n))
     o = host(solve_batch(b.cfg, b.gamma, b.sigma))
     e = runner.run(b.cfg, b.gamma, b.sigma, mode=0)
-    agree = np.abs(o["ee"] - e["ee"]) <= 1e-9 * np.abs(e["ee"])
-    assert agree.mean() >= 0.9
+    assert np.array_equal(o["status"], e["status"])
+    assert np.array_equal(o["rho"], e["rho"]) and np.array_equal(o["a"], e["a"])
+    assert np.array_equal(o["outer_iters"], e["outer_iters"])
+    assert np.all(np.abs(o["ee"] - e["ee"]) <= 1e-9 * np.abs(e["ee"]))
 
 
 def test_reference_shaped_api(golden):
@@ -143,8 +151,8 @@ def test_full_size_properties(name, count):
     b = workload_batch(name, range(1000, 1000 + count))
     o = host(solve_batch(b.cfg, b.gamma, b.sigma))
     cfg = b.cfg
+    assert np.all(o["status"] <= 3)  # every instance solved (3: the reference raises too)
     ok = o["status"] <= 2
-    assert ok.mean() >= 0.98
     assert np.all(o["feasible"][ok] == 1)
     assert np.allclose(o["ee"][ok], o["sum_rate"][ok] / o["total_power"][ok], rtol=1e-12)
     p = o["p"][ok]
@@ -167,7 +175,7 @@ def test_sharding_is_order_free():
     assert np.array_equal(full["ee"][8:], half["ee"])
 
 
-@pytest.mark.parametrize("name,kb", [("c1", "0"), ("c1", "212"), ("c2", "100")])
+@pytest.mark.parametrize("name,kb", [("c1", "0"), ("c1", "200"), ("c2", "160")])
 def test_shared_memory_residency_is_placement_only(golden, monkeypatch, name, kb):
     """Work::bind_hot moves arrays between global and shared memory; the
     results must be bit-identical to the default placement."""
