@@ -253,7 +253,9 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   char* slots1 = base + HEADER + flags_bytes(in->B) + order_bytes(in->B);
   char* slots2 = slots1 + (size_t)P.slots * P.per;
   if (cudaMemsetAsync(base, 0, HEADER, s) != cudaSuccess) return HCRAN_E_LAUNCH;
-  v.dense = P.dense_all ? 1 : 0; v.dense_ok = P.dense_ok; v.flag_int = flags; v.flag_in = nullptr;
+  // pass-1 floor-tie flags only when a second pass will re-solve the flagged instances
+  v.dense = P.dense_all ? 1 : 0; v.dense_ok = P.dense_ok; v.flag_int = P.grid2 ? flags : nullptr;
+  v.flag_in = nullptr;
   v.order = nullptr;
   int launches = 0;
   const char* ord_env = getenv("HCRAN_ORDER");

@@ -6,7 +6,7 @@
 #     source lines (the .ncu-rep and the source CSV exceed gpurun's 64 MiB)
 TAG=${1:-r02}; NB=${2:-2960}; CFG=${3:-c2}
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv \
+[ -n "$SKIP_LAUNCHES" ] || ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv \
     python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_${TAG}.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:hcran_solve_kernel -c 1 -o /tmp/full_${TAG} \
     python tools/ncu_one.py $CFG $NB > gpurun_out/ncu_full_${TAG}.log 2>&1
