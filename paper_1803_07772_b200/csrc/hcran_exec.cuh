@@ -43,12 +43,19 @@ struct DevEx {
     lane = tid & 31;
     nwarps = nthr >> 5;
     red = scratch + grp * 2 * nwarps;
+    whole = (int)blockDim.x == gsize;
   }
+  bool whole;  // the instance owns the CTA (named barriers 1..15 are free)
   __device__ __forceinline__ void sync() const {
     if (nthr == (int)blockDim.x) __syncthreads();
     else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthr) : "memory");
   }
   __device__ __forceinline__ void wsync() const { __syncwarp(); }
+  // named barrier over `count` threads (a group of warps of one instance);
+  // id 1..15 (only when the instance owns the whole CTA)
+  __device__ __forceinline__ void gsync(int id, int count) const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
   __device__ __forceinline__ bool any(bool p) const {
     if (nthr == (int)blockDim.x) return __syncthreads_or(p) != 0;
     const unsigned v = __any_sync(0xffffffffu, p);
@@ -101,9 +108,12 @@ struct DevEx {
 
 struct HostEx {
   int tid = 0, nthr = 1, warp = 0, lane = 0, nwarps = 1, grp = 0;
+  bool whole = false;
+  double* red = nullptr;
   static constexpr int WS = 1;
   void sync() const {}
   void wsync() const {}
+  void gsync(int, int) const {}
   bool any(bool p) const { return p; }
   double wsum(double v) const { return v; }
   double wmax(double v) const { return v; }

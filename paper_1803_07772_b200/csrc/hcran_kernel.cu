@@ -318,12 +318,11 @@ extern "C" int32_t hcran_b200_last_launches(void) { return g_last_launches; }
 // phase profiler readout (only meaningful in a -DHCRAN_PROFILE build)
 extern "C" int hcran_b200_phase_cycles(unsigned long long* out32, int reset) {
 #if defined(HCRAN_PROFILE)
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(unsigned long long) * 32);
-  if (reset) {
-    unsigned long long z[32] = {0};
-    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-  }
+  // each kernel translation unit has its own counters: sum them
+  unsigned long long a[32], b[32];
+  phase_cycles_256(a, reset);
+  phase_cycles_512(b, reset);
+  for (int i = 0; i < 32; ++i) out32[i] = a[i] + b[i];
   return 0;
 #else
   for (int i = 0; i < 32; ++i) out32[i] = 0;

@@ -58,8 +58,11 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 
-// one getter per instantiated shape (defined in hcran_k<NT>.cu)
+// one getter per instantiated shape (defined in hcran_k<NT>.cu), and its
+// translation unit's phase-profiler counters (-DHCRAN_PROFILE builds)
 KernelFn kernel_256_256();
 KernelFn kernel_512_512();
+void phase_cycles_256(unsigned long long* out32, int reset);
+void phase_cycles_512(unsigned long long* out32, int reset);
 
 }  // namespace hcran
