@@ -40,7 +40,10 @@ __global__ void __launch_bounds__(NT, 1)
   W.layout(ws + slot * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0, GT / 32);
   extern __shared__ __align__(16) char hot_smem[];
   if (hot) W.bind_hot(hot_smem + ex.grp * hot_per, hot, v.M, v.K, v.N);  // generic pointers
+  W.fast = v.fast;
+  if (v.fast) W.fs = hot_smem + v.fs_off + (size_t)ex.grp * (GT / 32) * W.fs_stride;
   Solver<DevEx> S(ex, v, W, ctl);
+  S.fast_init();
   for (;;) {
     if (ex.tid == 0) next_s[ex.grp] = (long long)atomicAdd(counter, 1);
     ex.sync();

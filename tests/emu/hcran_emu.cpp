@@ -10,6 +10,11 @@
 #include "../../paper_1803_07772_b200/csrc/hcran_solver.cuh"
 
 using namespace hcran;
+// the staged per-subcarrier analysis (the device default) unless HCRAN_EMU_FAST=0
+static int emu_fast() {
+  const char* e = getenv("HCRAN_EMU_FAST");
+  return e ? atoi(e) : 2;
+}
 
 extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in_t* in,
                                hcran_batch_out_t* out, int mode, int64_t first, int64_t count,
@@ -20,7 +25,9 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   if (!base) return -1;
   memset(base, 0, bytes);
   W.layout(base, prob->M, prob->K, prob->N, true, 1);
+  W.fast = emu_fast();
   View v;
+  memset(&v, 0, sizeof(v));
   v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
   v.p_max = prob->p_max; v.mask = prob->p_mask; v.eta = prob->eta; v.w = prob->weights;
   v.sig = prob->sigma; v.static_power = prob->static_power; v.tol = prob->tol;
@@ -33,6 +40,7 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   Ctl ctl;
   memset(&ctl, 0, sizeof(ctl));
   Solver<HostEx> S(ex, v, W, ctl);
+  S.fast_init();
   // seated-pair SIC family with floor ties re-run dense in place (dense_off: no
   // re-run, to expose the seated model); HCRAN_SIC_DENSE: dense everywhere
   v.dense = (prob->sic_mode == HCRAN_SIC_DENSE) ? 1 : 0;
@@ -110,6 +118,7 @@ extern "C" int hcran_emu_sweep_snapshot(const hcran_problem_t* prob, const hcran
   char* base = (char*)aligned_alloc(256, (bytes + 255) & ~size_t(255));
   memset(base, 0, bytes);
   W.layout(base, prob->M, prob->K, prob->N, true, 1);
+  W.fast = emu_fast();
   View v;
   memset(&v, 0, sizeof(v));
   v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
@@ -122,6 +131,7 @@ extern "C" int hcran_emu_sweep_snapshot(const hcran_problem_t* prob, const hcran
   Ctl ctl;
   memset(&ctl, 0, sizeof(ctl));
   Solver<HostEx> S(ex, v, W, ctl);
+  S.fast_init();
   const int M = prob->M, K = prob->K, N = prob->N, C = M * K * N, P = K * (K - 1) / 2;
   S.load_instance(0);
   S.ctx_setup(0.0);

@@ -8,7 +8,7 @@ TAG=${1:-r02}; NB=${2:-2960}; CFG=${3:-c2}
 mkdir -p gpurun_out
 [ -n "$SKIP_LAUNCHES" ] || ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv \
     python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_${TAG}.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:hcran_solve_kernel -c 1 -o /tmp/full_${TAG} \
+ncu -f --set full --import-source on --clock-control none -k regex:hcran_solve_kernel -c 1 -o /tmp/full_${TAG} \
     python tools/ncu_one.py $CFG $NB > gpurun_out/ncu_full_${TAG}.log 2>&1
 ncu -i /tmp/full_${TAG}.ncu-rep --page raw --csv > gpurun_out/ncu_full_${TAG}_${CFG}_b${NB}_raw.csv 2>/dev/null
 ncu -i /tmp/full_${TAG}.ncu-rep --page details --csv > gpurun_out/ncu_full_${TAG}_${CFG}_b${NB}_details.csv 2>/dev/null

@@ -21,12 +21,13 @@ o = solve_batch(b.cfg, b.gamma, b.sigma)
 lib.hcran_b200_phase_cycles(out, 0)
 # thread 0 (warp 0) clock per phase; marks 1-5 are warp 0's own subcarriers
 names = {0: 'sw:products', 1: 'an:tables+full+utot', 2: 'an:columns (psi, own)', 3: 'an:dense family',
-         4: 'an:num/den', 24: 'sw:analyze tail',
+         4: 'an:num/den', 12: 'fast:stage', 13: 'fast:rows', 14: 'fast:columns', 15: 'fast:seats+own',
+         20: 'fast:num/den', 21: 'fast:tail', 24: 'sw:analyze tail',
          25: 'sw:dense update', 26: 'sw:budget multiplier', 7: 'sw:closed form+zeta', 8: 'sw:convergence',
          10: 'round_start', 11: 'round end (surrogate, stops)',
          16: 'inner:setup', 17: 'inner:rounds', 18: 'inner:repair', 19: 'inner:feasible',
          27: 'repair:prune+rescale', 28: 'repair:trim', 29: 'repair:boost', 30: 'repair:sic_cleanup', 31: 'repair:final rates'}
-tot = sum(out[i] for i in (0, 1, 2, 3, 4, 24, 25, 26, 7, 8)) or 1
+tot = sum(out[i] for i in (0, 1, 2, 3, 4, 12, 13, 14, 15, 20, 21, 24, 25, 26, 7, 8)) or 1
 print('sweeps', int(o['sweeps'].sum().item()), 'instances', nb)
 for i in range(32):
     if out[i]:
