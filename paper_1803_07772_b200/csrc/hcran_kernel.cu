@@ -181,8 +181,8 @@ static void choose_hot(const hcran_problem_t* prob, int maxsm, Plan* P) {
   // staged analysis (Solver::analyze_fast): one scratch per warp after the hot arrays
   const char* fe = getenv("HCRAN_FAST");
   P->fs_off = (P->hot_smem + 15) & ~(size_t)15;
-  const size_t fs = (size_t)(P->sh.nt / 32) * Work::fs_bytes(prob->M, prob->K);
-  P->fast = (P->fs_off + fs <= cap) ? (fe ? atoi(fe) : 2) : 0;
+  const size_t fs = Work::fs_bytes(prob->M, prob->K, Work::fs_block(prob->K, prob->N, P->sh.gt));
+  P->fast = (P->groups == 1 && P->fs_off + fs <= cap) ? (fe ? atoi(fe) : 1) : 0;
   P->dyn_smem = P->fast ? P->fs_off + fs : P->hot_smem;
   if (P->dyn_smem) cudaFuncSetAttribute(kernel_of(P->sh), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)P->dyn_smem);

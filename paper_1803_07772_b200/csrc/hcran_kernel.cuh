@@ -11,6 +11,7 @@
 // sweeps) is absorbed by the queue.
 #pragma once
 #include <cuda_runtime.h>
+#include <new>
 #include "hcran_solver.cuh"
 
 namespace hcran {
@@ -32,17 +33,28 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ double red[2 * NT / 32];
   __shared__ Ctl ctl_s[G];
   __shared__ long long next_s[G];
+  // The workspace pointer table (Work, ~1 KB) and the problem view are
+  // uniform over the instance's threads: one copy in shared memory (broadcast
+  // loads) instead of a per-thread copy in local memory, which at 512 threads
+  // is ~0.7 MB of stack per SM and misses L1 on every array base fetch.
+  __shared__ __align__(16) unsigned char work_s[G][sizeof(Work)];
+  __shared__ View view_s;
   DevEx ex;
   ex.init(red, GT);
   Ctl& ctl = ctl_s[ex.grp];
-  Work W;
-  const size_t slot = (size_t)blockIdx.x * G + ex.grp;
-  W.layout(ws + slot * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0, GT / 32);
+  Work& W = *reinterpret_cast<Work*>(work_s[ex.grp]);
   extern __shared__ __align__(16) char hot_smem[];
-  if (hot) W.bind_hot(hot_smem + ex.grp * hot_per, hot, v.M, v.K, v.N);  // generic pointers
-  W.fast = v.fast;
-  if (v.fast) W.fs = hot_smem + v.fs_off + (size_t)ex.grp * (GT / 32) * W.fs_stride;
-  Solver<DevEx> S(ex, v, W, ctl);
+  if (threadIdx.x == 0) view_s = v;
+  if (ex.tid == 0) {
+    new (&W) Work();
+    const size_t slot = (size_t)blockIdx.x * G + ex.grp;
+    W.layout(ws + slot * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0, GT / 32);
+    if (hot) W.bind_hot(hot_smem + ex.grp * hot_per, hot, v.M, v.K, v.N);  // generic pointers
+    W.fast = v.fast;
+    if (v.fast) W.fs = hot_smem + v.fs_off;  // one instance per CTA (GT == NT) when fast
+  }
+  __syncthreads();
+  Solver<DevEx> S(ex, view_s, W, ctl);
   S.fast_init();
   for (;;) {
     if (ex.tid == 0) next_s[ex.grp] = (long long)atomicAdd(counter, 1);

@@ -85,8 +85,8 @@ struct Work {
   double *gT, *aT;
   uint8_t* rT;
   int tsd = 0, tsb = 0;
-  char* fs = nullptr;   // per-warp analysis scratch (shared memory on the device)
-  int fs_stride = 0;    // its bytes per warp
+  char* fs = nullptr;   // staged-analysis scratch of the CTA (shared memory on the device)
+  int fs_nb = 1;        // subcarriers per staged block
   int fast = 0;         // analyze_fast is bound (the scratch fits)
 
   double* wleaf;    // [nw][wlstride]: leaf sums of the warp-parallel pairwise sums
@@ -101,16 +101,22 @@ struct Work {
   HD static int t_kp(int K) { return K | 1; }
   HD static int t_sd(int M, int K) { return (M * t_kp(K) + 1) & ~1; }
   HD static int t_sb(int M, int K) { return (M * t_kp(K) + 15) & ~15; }
-  // per-warp scratch of the staged analysis (FsView below)
-  HD static size_t fs_bytes(int M, int K) {
+  // CTA scratch of the staged analysis (Solver::FsView): two stages of NB
+  // subcarrier blocks plus the block's u_tot / received power / psi_cross terms
+  HD static size_t fs_bytes(int M, int K, int NB) {
     const size_t a16 = 15;
-    size_t b = 16;                                   // mbarrier + phase
-    b += 2 * (size_t)t_sd(M, K) * 8;                 // G, U (alpha -> u)
-    b += ((size_t)t_sb(M, K) + a16) & ~a16;          // R
-    b += 2 * (((size_t)K * 8 + a16) & ~a16);         // UT, FL
-    b += (size_t)M * 8 * (6 + SMAX + (SMAX + 1));    // TT PA PB FT PC spare, PS, CQ
-    b += ((size_t)M * SMAX + a16) & ~a16;            // CR
+    size_t b = 32;                                              // 2 mbarriers + 2 phases
+    b += 2 * (2 * (size_t)NB * t_sd(M, K) * 8 + (size_t)NB * t_sb(M, K));
+    b += 2 * (((size_t)NB * K * 8 + a16) & ~a16);               // UT, FL
+    b += 2 * (((size_t)NB * M * 8 + a16) & ~a16);               // PA, PB
     return (b + a16) & ~a16;
+  }
+  // subcarriers per block: one row (k, n) per thread
+  HD static int fs_block(int K, int N, int nthr) {
+    int nb = nthr / K;
+    if (nb > 16) nb = 16;
+    if (nb > N) nb = N;
+    return nb < 1 ? 1 : nb;
   }
   // seats per user the per-user lists hold: a user may sit on several heads
   // only in small instances (multistart / external warm starts)
@@ -178,8 +184,8 @@ struct Work {
     tsd = t_sd(M, K);
     tsb = t_sb(M, K);
     HC_D(gT, (size_t)tsd * N); HC_D(aT, (size_t)tsd * N); HC_B(rT, (size_t)tsb * N);
-    fs_stride = (int)fs_bytes(M, K);
-    fs = take((size_t)fs_stride * nw);
+    fs_nb = fs_block(K, N, 32 * nw);
+    fs = take(fs_bytes(M, K, fs_nb));
     HC_B(ord, C); HC_B(rnk, C); HC_B(slot, C); HC_B(flag, C);
     HC_B(cs_r, MN * SMAX); HC_D(cs_q, MN * (SMAX + 1));
     HC_D(wleaf, size_t(nw) * wlstride); HC_I(wleafi, size_t(nw) * wlstride);

@@ -13,7 +13,7 @@ using namespace hcran;
 // the staged per-subcarrier analysis (the device default) unless HCRAN_EMU_FAST=0
 static int emu_fast() {
   const char* e = getenv("HCRAN_EMU_FAST");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 1;
 }
 
 extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in_t* in,
