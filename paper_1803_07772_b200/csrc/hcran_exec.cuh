@@ -13,7 +13,6 @@
 #pragma once
 #include <stdint.h>
 #include <math.h>
-#include <string.h>
 
 #if defined(__CUDACC__)
 #define HD __host__ __device__
@@ -85,47 +84,6 @@ struct DevEx {
     return v;
   }
   __device__ __forceinline__ bool wany(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
-  // ---- bulk async copies (TMA, cp.async.bulk) into this warp's shared scratch,
-  // completed on an mbarrier (one per warp; lane 0 issues, every lane waits)
-  static __device__ __forceinline__ unsigned saddr(const void* p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-  }
-  __device__ __forceinline__ void bulk_init(uint64_t* mb) const {
-    if (lane == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(mb)) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncwarp();
-  }
-  // order this thread's generic-proxy accesses (global and shared) before
-  // later async-proxy (bulk copy) accesses issued after a barrier
-  __device__ __forceinline__ void fence_async() const { asm volatile("fence.proxy.async;" ::: "memory"); }
-  __device__ __forceinline__ void fence_async_smem() const {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __device__ __forceinline__ void bulk_expect(uint64_t* mb, unsigned bytes) const {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(mb)), "r"(bytes)
-                 : "memory");
-  }
-  __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
-                                            uint64_t* mb) const {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            saddr(dst)),
-        "l"(src), "r"(bytes), "r"(saddr(mb))
-        : "memory");
-  }
-  __device__ __forceinline__ void bulk_wait(uint64_t* mb, unsigned phase) const {
-    unsigned done = 0;
-    while (!done) {
-      asm volatile(
-          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-          : "=r"(done)
-          : "r"(saddr(mb)), "r"(phase)
-          : "memory");
-    }
-  }
   // group-level (all threads receive the result; deterministic order)
   __device__ double sum(double v) const {
     v = wsum(v);
@@ -161,12 +119,6 @@ struct HostEx {
   double wmax(double v) const { return v; }
   int wmaxi(int v) const { return v; }
   bool wany(bool p) const { return p; }
-  void bulk_init(uint64_t*) const {}
-  void fence_async() const {}
-  void fence_async_smem() const {}
-  void bulk_expect(uint64_t*, unsigned) const {}
-  void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t*) const { memcpy(dst, src, bytes); }
-  void bulk_wait(uint64_t*, unsigned) const {}
   double sum(double v) const { return v; }
   double max(double v) const { return v; }
 };

@@ -143,9 +143,6 @@ struct Plan {
   unsigned hot;      // Work::HOT_* arrays bound to dynamic shared memory
   size_t hot_smem;   // their bytes per CTA
   size_t hot_per;    // ... per instance (thread group)
-  size_t fs_off;     // staged-analysis scratch: offset in dynamic shared memory
-  size_t dyn_smem;   // dynamic shared memory per CTA (hot arrays + scratch)
-  int fast;          // 1: the staged analysis runs (its scratch fits)
   Shape sh;          // launch shape
   int groups;        // instances per CTA
   int dense_all;     // 1: every instance runs the dense SIC pair family in pass 1
@@ -178,14 +175,8 @@ static void choose_hot(const hcran_problem_t* prob, int maxsm, Plan* P) {
     P->hot_per += b;
   }
   P->hot_smem = P->hot_per * P->groups;
-  // staged analysis (Solver::analyze_fast): one scratch per warp after the hot arrays
-  const char* fe = getenv("HCRAN_FAST");
-  P->fs_off = (P->hot_smem + 15) & ~(size_t)15;
-  const size_t fs = Work::fs_bytes(prob->M, prob->K, Work::fs_block(prob->K, prob->N, P->sh.gt));
-  P->fast = (P->groups == 1 && P->fs_off + fs <= cap) ? (fe ? atoi(fe) : 1) : 0;
-  P->dyn_smem = P->fast ? P->fs_off + fs : P->hot_smem;
-  if (P->dyn_smem) cudaFuncSetAttribute(kernel_of(P->sh), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)P->dyn_smem);
+  if (P->hot_smem) cudaFuncSetAttribute(kernel_of(P->sh), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)P->hot_smem);
 }
 
 static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P) {
@@ -204,7 +195,7 @@ static int make_plan(const hcran_problem_t* prob, int64_t B, int device, Plan* P
   P->dense_all = prob->sic_mode == HCRAN_SIC_DENSE ? 1 : 0;
   if (dn) P->dense_all = atoi(dn);
   choose_hot(prob, maxsm, P);
-  int64_t g = resident_ctas(device, P->sh, P->dyn_smem);
+  int64_t g = resident_ctas(device, P->sh, P->hot_smem);
   const int64_t gneed = (Bp + P->groups - 1) / P->groups;
   if (g > gneed) g = gneed;
   P->grid = g;
@@ -266,8 +257,6 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
   v.dense = P.dense_all ? 1 : 0; v.dense_ok = P.dense_ok; v.flag_int = P.grid2 ? flags : nullptr;
   v.flag_in = nullptr;
   v.order = nullptr;
-  v.fast = P.fast;
-  v.fs_off = (int)P.fs_off;
   int launches = 0;
   const char* ord_env = getenv("HCRAN_ORDER");
   if (in->B > P.slots && !(ord_env && atoi(ord_env) == 0)) {  // queue order matters past one wave
@@ -280,14 +269,14 @@ static int launch(const hcran_problem_t* prob, const hcran_batch_in_t* in, hcran
     launches = 3;
   }
   const KernelFn kfn = kernel_of(P.sh);
-  kfn<<<(unsigned)P.grid, P.sh.nt, P.dyn_smem, s>>>(v, slots1, P.per, (int*)base, mode, P.hot, P.hot_per);
+  kfn<<<(unsigned)P.grid, P.sh.nt, P.hot_smem, s>>>(v, slots1, P.per, (int*)base, mode, P.hot, P.hot_per);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   if (P.grid2 == 0) {  // pass 1 already settled every floor tie (or the fast model ignores them)
     g_last_launches = launches + 1;
     return HCRAN_OK;
   }
   v.dense = 1; v.dense_ok = 0; v.flag_int = nullptr; v.flag_in = flags;
-  kfn<<<(unsigned)P.grid2, P.sh.nt, P.dyn_smem, s>>>(v, slots2, P.perd, (int*)base + 1, mode, P.hot,
+  kfn<<<(unsigned)P.grid2, P.sh.nt, P.hot_smem, s>>>(v, slots2, P.perd, (int*)base + 1, mode, P.hot,
                                                      P.hot_per);
   if (cudaGetLastError() != cudaSuccess) return HCRAN_E_LAUNCH;
   g_last_launches = launches + 2;
@@ -302,7 +291,7 @@ extern "C" int hcran_b200_engine(const hcran_problem_t* prob, int64_t B, int dev
   make_plan(prob, B, device, &P);
   if (engine) *engine = 0;   // one CTA per instance (the cluster engine of round 1 is gone)
   if (cluster) *cluster = 1;
-  if (smem) *smem = P.dyn_smem;
+  if (smem) *smem = P.hot_smem;
   return HCRAN_OK;
 }
 

@@ -50,12 +50,9 @@ __global__ void __launch_bounds__(NT, 1)
     const size_t slot = (size_t)blockIdx.x * G + ex.grp;
     W.layout(ws + slot * per_cta, v.M, v.K, v.N, v.dense != 0 || v.dense_ok != 0, GT / 32);
     if (hot) W.bind_hot(hot_smem + ex.grp * hot_per, hot, v.M, v.K, v.N);  // generic pointers
-    W.fast = v.fast;
-    if (v.fast) W.fs = hot_smem + v.fs_off;  // one instance per CTA (GT == NT) when fast
   }
   __syncthreads();
   Solver<DevEx> S(ex, view_s, W, ctl);
-  S.fast_init();
   for (;;) {
     if (ex.tid == 0) next_s[ex.grp] = (long long)atomicAdd(counter, 1);
     ex.sync();

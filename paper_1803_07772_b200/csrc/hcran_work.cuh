@@ -79,16 +79,6 @@ struct Work {
   double* pbest;                                   // [C] multistart: best start's end point
   double *robj, *robj_best;                        // [RMAX] round objectives (current / accepted start)
 
-  // subcarrier-major copies for the staged analysis (Solver::analyze_fast):
-  // [n][m*KP + k], tsd doubles / tsb bytes per subcarrier (16-byte multiples,
-  // so one subcarrier's block is one bulk async copy)
-  double *gT, *aT;
-  uint8_t* rT;
-  int tsd = 0, tsb = 0;
-  char* fs = nullptr;   // staged-analysis scratch of the CTA (shared memory on the device)
-  int fs_nb = 1;        // subcarriers per staged block
-  int fast = 0;         // analyze_fast is bound (the scratch fits)
-
   double* wleaf;    // [nw][wlstride]: leaf sums of the warp-parallel pairwise sums
   int32_t* wleafi;  // [nw][wlstride]: their offsets (PwCache)
   int wlstride;
@@ -96,28 +86,6 @@ struct Work {
   double* gam_hot = nullptr;  // shared-memory copy of the instance's gains (bound by the kernel, else null)
 
   HD static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
-  // rows m of a subcarrier block are KP = K | 1 apart (odd: the column pass's
-  // lanes, one per m, hit distinct shared-memory banks)
-  HD static int t_kp(int K) { return K | 1; }
-  HD static int t_sd(int M, int K) { return (M * t_kp(K) + 1) & ~1; }
-  HD static int t_sb(int M, int K) { return (M * t_kp(K) + 15) & ~15; }
-  // CTA scratch of the staged analysis (Solver::FsView): two stages of NB
-  // subcarrier blocks plus the block's u_tot / received power / psi_cross terms
-  HD static size_t fs_bytes(int M, int K, int NB) {
-    const size_t a16 = 15;
-    size_t b = 32;                                              // 2 mbarriers + 2 phases
-    b += 2 * (2 * (size_t)NB * t_sd(M, K) * 8 + (size_t)NB * t_sb(M, K));
-    b += 2 * (((size_t)NB * K * 8 + a16) & ~a16);               // UT, FL
-    b += 2 * (((size_t)NB * M * 8 + a16) & ~a16);               // PA, PB
-    return (b + a16) & ~a16;
-  }
-  // subcarriers per block: one row (k, n) per thread
-  HD static int fs_block(int K, int N, int nthr) {
-    int nb = nthr / K;
-    if (nb > 16) nb = 16;
-    if (nb > N) nb = N;
-    return nb < 1 ? 1 : nb;
-  }
   // seats per user the per-user lists hold: a user may sit on several heads
   // only in small instances (multistart / external warm starts)
   HD static int useat_cap(int M, int K, int N) {
@@ -181,11 +149,6 @@ struct Work {
 #define HC_B(name, n) name = (uint8_t*)take(n)
 #define HC_I(name, n) name = (int32_t*)take(sizeof(int32_t) * (n))
     HC_D(p, C); HC_D(pacc, C); HC_D(alpha, C); HC_D(u, C);
-    tsd = t_sd(M, K);
-    tsb = t_sb(M, K);
-    HC_D(gT, (size_t)tsd * N); HC_D(aT, (size_t)tsd * N); HC_B(rT, (size_t)tsb * N);
-    fs_nb = fs_block(K, N, 32 * nw);
-    fs = take(fs_bytes(M, K, fs_nb));
     HC_B(ord, C); HC_B(rnk, C); HC_B(slot, C); HC_B(flag, C);
     HC_B(cs_r, MN * SMAX); HC_D(cs_q, MN * (SMAX + 1));
     HC_D(wleaf, size_t(nw) * wlstride); HC_I(wleafi, size_t(nw) * wlstride);

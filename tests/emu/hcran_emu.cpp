@@ -10,11 +10,6 @@
 #include "../../paper_1803_07772_b200/csrc/hcran_solver.cuh"
 
 using namespace hcran;
-// the staged per-subcarrier analysis (the device default) unless HCRAN_EMU_FAST=0
-static int emu_fast() {
-  const char* e = getenv("HCRAN_EMU_FAST");
-  return e ? atoi(e) : 1;
-}
 
 extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in_t* in,
                                hcran_batch_out_t* out, int mode, int64_t first, int64_t count,
@@ -25,7 +20,6 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   if (!base) return -1;
   memset(base, 0, bytes);
   W.layout(base, prob->M, prob->K, prob->N, true, 1);
-  W.fast = emu_fast();
   View v;
   memset(&v, 0, sizeof(v));
   v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
@@ -40,7 +34,6 @@ extern "C" int hcran_emu_solve(const hcran_problem_t* prob, const hcran_batch_in
   Ctl ctl;
   memset(&ctl, 0, sizeof(ctl));
   Solver<HostEx> S(ex, v, W, ctl);
-  S.fast_init();
   // seated-pair SIC family with floor ties re-run dense in place (dense_off: no
   // re-run, to expose the seated model); HCRAN_SIC_DENSE: dense everywhere
   v.dense = (prob->sic_mode == HCRAN_SIC_DENSE) ? 1 : 0;
@@ -118,7 +111,6 @@ extern "C" int hcran_emu_sweep_snapshot(const hcran_problem_t* prob, const hcran
   char* base = (char*)aligned_alloc(256, (bytes + 255) & ~size_t(255));
   memset(base, 0, bytes);
   W.layout(base, prob->M, prob->K, prob->N, true, 1);
-  W.fast = emu_fast();
   View v;
   memset(&v, 0, sizeof(v));
   v.M = prob->M; v.K = prob->K; v.N = prob->N; v.L = prob->l_max;
@@ -131,7 +123,6 @@ extern "C" int hcran_emu_sweep_snapshot(const hcran_problem_t* prob, const hcran
   Ctl ctl;
   memset(&ctl, 0, sizeof(ctl));
   Solver<HostEx> S(ex, v, W, ctl);
-  S.fast_init();
   const int M = prob->M, K = prob->K, N = prob->N, C = M * K * N, P = K * (K - 1) / 2;
   S.load_instance(0);
   S.ctx_setup(0.0);

@@ -82,32 +82,3 @@ def test_emu_warm_start_never_worse(golden):
     warm_obj = first["sum_rate"] - e * first["total_power"]
     assert np.all(second["objective"] >= warm_obj - 1e-9)
 
-
-def _run_with_fast(flag, name, draws, mode=0, dense_off=False):
-    import os
-    b = workload_batch(name, draws)
-    kw = dict(elastic=b.elastic, min_rates=b.min_rates, e_fixed=b.e_fixed) if mode == 1 else {}
-    old = os.environ.get("HCRAN_EMU_FAST")
-    os.environ["HCRAN_EMU_FAST"] = flag
-    try:
-        return runner.run(b.cfg, b.gamma, b.sigma, mode=mode, dense_off=dense_off, **kw)
-    finally:
-        if old is None:
-            del os.environ["HCRAN_EMU_FAST"]
-        else:
-            os.environ["HCRAN_EMU_FAST"] = old
-
-
-@pytest.mark.parametrize("name,draws,mode,dense_off", [
-    ("c0", range(64), 0, False), ("c1", range(24), 0, False), ("c1", range(24, 40), 0, True),
-    ("c4", range(64), 1, False), ("c2", range(2), 0, False)])
-def test_staged_analysis_is_bit_identical(name, draws, mode, dense_off):
-    """The per-subcarrier staged analysis (analyze_fast: one warp per
-    subcarrier, bulk-copied gains / slopes / ranks, u and u_tot in shared
-    memory) is a placement change only: every output equals the CTA-phase
-    path's bit for bit."""
-    off = _run_with_fast("0", name, draws, mode, dense_off)
-    for variant in ("1",):
-        on = _run_with_fast(variant, name, draws, mode, dense_off)
-        for k in on:
-            assert np.array_equal(on[k], off[k], equal_nan=on[k].dtype.kind == "f"), (variant, k)
