@@ -61,6 +61,7 @@ struct Work {
   // repair scratch
   double *tb, *tX, *tY, *tS, *leaf;  // [MN] x4, leaf [C/64 + 64]
   int32_t* perm;                     // [N]
+  int32_t* tlist;                    // [MN + 64] trim: each lane's active columns (strided by the warp size)
   uint8_t *dmask, *tie;              // [N] subcarriers on the dense SIC family / with a floor tie
   // repair: the nonzero cells of each column (<= l_max after the top-l cut),
   // users in index order (nzu) and in decode order (nzr); nzc 255 = not sparse
@@ -173,7 +174,7 @@ struct Work {
     HC_D(xi, M); HC_D(delta, M); HC_D(eps1, M); HC_D(eps2, M); HC_D(mtmp, M);
     HC_I(mev, M);
     HC_D(tb, MN); HC_D(tX, MN); HC_D(tY, MN); HC_D(tS, MN); HC_D(leaf, C / 64 + 64);
-    HC_I(perm, N);
+    HC_I(perm, N); HC_I(tlist, MN + 64);
     HC_B(dmask, N); HC_B(tie, N); HC_I(dlist, N);
     HC_B(nzu, MN * SMAX); HC_B(nzr, MN * SMAX); HC_B(nzc, MN);
     HC_I(tq_col, TQMAX); HC_B(tq_sm, TQMAX); HC_D(tq_val, TQMAX); HC_D(tq_step, TQMAX);
