@@ -84,14 +84,6 @@ struct DevEx {
     return v;
   }
   __device__ __forceinline__ bool wany(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
-  // 64-bit mask updates shared by threads of the instance
-  static __device__ __forceinline__ void or64(uint64_t* a, uint64_t v) {
-    atomicOr((unsigned long long*)a, (unsigned long long)v);
-  }
-  static __device__ __forceinline__ void and64(uint64_t* a, uint64_t v) {
-    atomicAnd((unsigned long long*)a, (unsigned long long)v);
-  }
-  static __device__ __forceinline__ int lowbit64(uint64_t v) { return __ffsll((long long)v) - 1; }
   // group-level (all threads receive the result; deterministic order)
   __device__ double sum(double v) const {
     v = wsum(v);
@@ -127,9 +119,6 @@ struct HostEx {
   double wmax(double v) const { return v; }
   int wmaxi(int v) const { return v; }
   bool wany(bool p) const { return p; }
-  static void or64(uint64_t* a, uint64_t v) { *a |= v; }
-  static void and64(uint64_t* a, uint64_t v) { *a &= v; }
-  static int lowbit64(uint64_t v) { return __builtin_ctzll(v); }
   double sum(double v) const { return v; }
   double max(double v) const { return v; }
 };

@@ -70,7 +70,6 @@ struct Work {
   // dense SIC pair family (exact mode for floor-tie instances) -- bound when dense
   double *cx, *cxl, *dA, *dB, *nS, *nW, *dg, *ag;  // [C]
   double *pd_zt, *pd_step;                         // [K(K-1)/2][MN] (pair-major)
-  uint64_t* pd_nz;  // [C] (K <= 64): bit y of cell (m, x, n) set iff pair (x, y)'s multiplier is nonzero
   uint8_t *pq_i, *pq_j;                            // [K(K-1)/2] members of pair q
   // products-active families: tuple rows (column, slot mask) and cross-head seat pairs
   int32_t *tq_col, *th_a, *th_b;                   // [TQMAX], [THMAX] x2 (seat ids)
@@ -189,11 +188,9 @@ struct Work {
       HC_D(cx, C); HC_D(cxl, C); HC_D(dA, C); HC_D(dB, C); HC_D(nS, C); HC_D(nW, C);
       HC_D(dg, C); HC_D(ag, C);
       HC_D(pd_zt, PD); HC_D(pd_step, PD);
-      pd_nz = (uint64_t*)take(sizeof(uint64_t) * (K <= 64 ? C : 1));
       HC_B(pq_i, PD / MN + 1); HC_B(pq_j, PD / MN + 1);
     } else {
       cx = cxl = dA = dB = nS = nW = dg = ag = pd_zt = pd_step = nullptr;
-      pd_nz = nullptr;
       pq_i = pq_j = nullptr;
     }
 #undef HC_D
