@@ -84,6 +84,8 @@ struct DevEx {
     return v;
   }
   __device__ __forceinline__ bool wany(bool p) const { return __any_sync(0xffffffffu, p) != 0; }
+  static __device__ __forceinline__ int fetch_add(int* p, int v) { return atomicAdd(p, v); }
+  __device__ __forceinline__ int wbcast0(int v) const { return __shfl_sync(0xffffffffu, v, 0); }
   // group-level (all threads receive the result; deterministic order)
   __device__ double sum(double v) const {
     v = wsum(v);
@@ -119,6 +121,8 @@ struct HostEx {
   double wmax(double v) const { return v; }
   int wmaxi(int v) const { return v; }
   bool wany(bool p) const { return p; }
+  static int fetch_add(int* p, int v) { const int o = *p; *p += v; return o; }
+  int wbcast0(int v) const { return v; }
   double sum(double v) const { return v; }
   double max(double v) const { return v; }
 };
